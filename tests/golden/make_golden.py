@@ -1,0 +1,161 @@
+"""Generate golden fixtures by running the REAL reference (``baksolve`` 0.1.0).
+
+Run in the build container, where the reference is mounted read-only:
+
+    python tests/golden/make_golden.py            # writes tests/golden/*.npz
+
+The reference is imported from ``/root/reference/pkg/src`` (pure Python on
+numpy/OpenBLAS).  Nothing at test time reads ``/root/reference``: the
+fixtures committed next to this script carry everything the tests need.
+
+Each fixture stores the solve inputs either explicitly (small, or built with
+``np.random.default_rng`` as the reference's own tests do) or as a
+``generate_system`` spec plus a SHA-256 of the drawn bytes (so the oracle's
+generator restatement is pinned too), together with the reference's outputs:
+a_hat, residual, per-sweep history, sweeps_run, converged, drift_warning,
+and the fp64-recomputed residual norm of bench.py:180-184.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def main():
+    sys.path.insert(0, REF_SRC)
+    import baksolve as bk
+    from baksolve.bench import _predict_f64
+    from threadpoolctl import threadpool_info
+
+    np.dot(np.ones(2), np.ones(2))
+    blas = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+    host = {"numpy": np.__version__,
+            "blas": (blas[0].get("internal_api"), blas[0].get("version"),
+                     blas[0].get("architecture")) if blas else None}
+
+    cases = []
+
+    def add(name, x, y, cfg, a0=None, spec=None, store_inputs=True):
+        rep = bk.solve_bak(x, y, cfg, a0=a0)
+        pred = _predict_f64(x, rep.a_hat)
+        rnorm = float(np.linalg.norm(np.asarray(y, np.float64) - pred))
+        d = dict(
+            a_hat=rep.a_hat, residual=rep.residual,
+            history=np.asarray(rep.residual_norm_history if rep.residual_norm_history is not None else [], np.float64),
+            has_history=np.array(rep.residual_norm_history is not None),
+            sweeps_run=np.array(rep.sweeps_run), converged=np.array(rep.converged),
+            drift_warning=np.array(rep.drift_warning), resid_norm_f64=np.array(rnorm),
+            ynorm_f64=np.array(float(np.linalg.norm(np.asarray(y, np.float64)))),
+            max_iter=np.array(cfg.max_iter), tol=np.array(cfg.tol),
+            ordering=np.array(cfg.ordering), ordering_seed=np.array(cfg.ordering_seed),
+            record_history=np.array(cfg.record_history),
+            input_sha=np.array(_sha(np.asfortranarray(x), y)),
+            dtype=np.array(np.dtype(x.dtype).name),
+            shape=np.array(x.shape),
+            host=np.array(json.dumps(host)),
+            spec=np.array(json.dumps(spec) if spec else ""),
+        )
+        if a0 is not None:
+            d["a0"] = np.asarray(a0)
+        if store_inputs:
+            d["x"] = np.asfortranarray(x)
+            d["y"] = np.asarray(y)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+        cases.append(name)
+        print(f"{name:28s} {str(x.shape):>16s} {x.dtype} sweeps={rep.sweeps_run} "
+              f"conv={rep.converged} |r|={rnorm:.6e}")
+
+    SC = bk.SolveConfig
+
+    # --- known-answer tests of the reference suite (test_solver_bak.py) ---
+    add("kat_identity3", np.eye(3, order="F"), np.array([1.0, 2.0, 3.0]), SC(max_iter=1, tol=0))
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((60, 8)))
+    xo = np.asfortranarray(q * rng.uniform(0.5, 2.0, 8))
+    add("orthogonal_60x8", xo, rng.standard_normal(60), SC(max_iter=1, tol=0))
+    rng = np.random.default_rng(14)
+    xz = np.asfortranarray(rng.standard_normal((50, 4)))
+    xz[:, 2] = 0.0
+    yz = rng.standard_normal(50)
+    add("zero_column_50x4", xz, yz, SC(max_iter=200, tol=0))
+    add("zero_column_warm_50x4", xz, yz, SC(max_iter=50, tol=0), a0=np.array([0.0, 0.0, 7.5, 0.0]))
+    add("zero_target_4", np.eye(4, order="F"), np.zeros(4), SC(record_history=True))
+
+    # --- generated systems (pins generate_system too: spec + sha) ---
+    def gen(name, obs, nv, seed, prec, cfg, dist="normal", cdist="uniform", sigma=0.01, store=False):
+        spec = dict(obs=obs, vars=nv, seed=seed, distribution=dist,
+                    coeff_distribution=cdist, noise_sigma=sigma, precision=prec)
+        x, y, _ = bk.generate_system(bk.SystemSpec(obs=obs, vars=nv, seed=seed, distribution=dist,
+                                                   coeff_distribution=cdist, noise_sigma=sigma), prec)
+        add(name, x, y, cfg, spec=spec, store_inputs=store)
+
+    gen("c1_scaled_2000x40_f64", 2000, 40, 1, "double", SC(max_iter=100, tol=0, record_history=True))
+    gen("c1_full_10000x100_f64", 10_000, 100, 1, "double", SC(max_iter=100, tol=0, record_history=True))
+    gen("c1_scaled_2000x40_f32", 2000, 40, 1, "single", SC(max_iter=100, tol=0, record_history=True))
+    gen("early_break_1000x100_f32", 1000, 100, 5, "single", SC(max_iter=300, tol=1e-6, record_history=True),
+        dist="uniform", sigma=0.0)
+    gen("early_break_400x50_f64", 400, 50, 7, "double", SC(max_iter=5000, tol=1e-12, record_history=True),
+        dist="uniform", sigma=0.0)
+    gen("random_order_300x30_f64", 300, 30, 9, "double",
+        SC(max_iter=40, tol=1e-9, ordering="random", ordering_seed=11, record_history=True))
+    gen("random_order_300x30_f32", 300, 30, 9, "single",
+        SC(max_iter=40, tol=0, ordering="random", ordering_seed=12, record_history=True))
+    gen("c3_scaled_65536x64_f64", 65536, 64, 3, "double", SC(max_iter=5, tol=0, record_history=True))
+    gen("c3_scaled_65536x64_f32", 65536, 64, 3, "single", SC(max_iter=5, tol=0, record_history=True))
+    for s in range(4):
+        gen(f"c5_system{s}_512x32_f32", 512, 32, 5_000_000 + s, "single", SC(max_iter=200, tol=0))
+
+    # --- wide / square / ragged / degenerate, explicit inputs ---
+    rng = np.random.default_rng(1001)
+    xw = np.asfortranarray(rng.standard_normal((40, 100)))
+    add("wide_40x100_f64", xw, xw @ rng.standard_normal(100), SC(max_iter=50, tol=1e-6, record_history=True))
+    rng = np.random.default_rng(1002)
+    xs = np.asfortranarray(rng.standard_normal((80, 80)).astype(np.float32))
+    ys = (xs @ rng.standard_normal(80).astype(np.float32) + 0.5 * rng.standard_normal(80)).astype(np.float32)
+    add("square_noisy_80x80_f32", xs, ys,
+        SC(max_iter=50, tol=1e-6, ordering="random", ordering_seed=3, record_history=True))
+    rng = np.random.default_rng(10)
+    xr = np.asfortranarray(rng.standard_normal((37, 9)).astype(np.float32))
+    add("ragged_37x9_f32", xr, rng.standard_normal(37).astype(np.float32), SC(max_iter=60, tol=0, record_history=True))
+    rng = np.random.default_rng(8)
+    x8 = np.asfortranarray(rng.standard_normal((120, 20)).astype(np.float32))
+    y8 = (x8 @ rng.standard_normal(20).astype(np.float32) + 0.2 * rng.standard_normal(120)).astype(np.float32)
+    add("stagnation_120x20_f32", x8, y8, SC(max_iter=800, tol=0, record_history=True))
+    rng = np.random.default_rng(21)
+    x1 = np.asfortranarray(rng.standard_normal((33, 1)))
+    add("single_column_33x1_f64", x1, rng.standard_normal(33), SC(max_iter=3, tol=0, record_history=True))
+    rng = np.random.default_rng(22)
+    xc2 = rng.standard_normal(256 * 256).reshape((256, 256), order="F") / 16.0
+    xc2[np.arange(256), np.arange(256)] += 4.0
+    yc2 = xc2 @ (rng.random(256) * 2 - 1)
+    add("c2_scaled_256_f64", xc2, yc2, SC(max_iter=50, tol=0, record_history=True))
+    add("c2_scaled_256_f64_break", xc2, yc2, SC(max_iter=50, tol=1e-10, record_history=True))
+    rng = np.random.default_rng(23)
+    xc4 = np.asfortranarray(rng.standard_normal((100, 3000)))
+    add("c4_scaled_100x3000_f64", xc4, rng.standard_normal(100), SC(max_iter=10, tol=0, record_history=True))
+
+    # coordinate_update KAT (test_solver_bak.py:17-20)
+    da, e_next = bk.coordinate_update(np.array([1.0, 2.0]), np.array([3.0, 4.0]))
+    np.savez_compressed(os.path.join(HERE, "kat_coordinate_update.npz"),
+                        col=np.array([1.0, 2.0]), e=np.array([3.0, 4.0]), da=np.array(da), e_next=e_next)
+    with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
+        json.dump({"host": host, "cases": cases, "reference": "baksolve 0.1.0 (/root/reference/pkg)"}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,40 @@
+"""Load the committed golden fixtures (tests/golden/*.npz, made by
+tests/golden/make_golden.py from the real reference)."""
+
+import glob
+import json
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("kat_coordinate"))
+
+
+def load(name):
+    with np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    spec = str(d["spec"])
+    if "x" not in d:
+        from oracle import bak_oracle as orc
+        s = json.loads(spec)
+        x, y, _ = orc.make_system(s["obs"], s["vars"], s["seed"], s["distribution"],
+                                  s["coeff_distribution"], s["noise_sigma"], s["precision"])
+        d["x"], d["y"] = x, y
+    d["config"] = dict(max_iter=int(d["max_iter"]), tol=float(d["tol"]), ordering=str(d["ordering"]),
+                       ordering_seed=int(d["ordering_seed"]), record_history=bool(d["record_history"]))
+    d["a0"] = d.get("a0")
+    d["host"] = json.loads(str(d["host"]))
+    return d
+
+
+def input_sha(x, y):
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(np.asfortranarray(x)).tobytes())
+    h.update(np.ascontiguousarray(y).tobytes())
+    return h.hexdigest()

@@ -1,0 +1,142 @@
+/*
+ * bak200 — B200-native (sm_100a) SolveBak column sweep, C ABI.
+ *
+ * The reference (baksolve 0.1.0, /root/reference/pkg) is pure Python and has
+ * no FFI: its operator API for this path is the Python call
+ *     baksolve.bak.solve_bak(x, y, config, a0) -> SolveReport   (bak.py:146-195)
+ * Each entry point below replaces one piece of that call, so a maintainer
+ * binds them with ctypes exactly as paper_2104_12570_b200
+ * does.  All pointers are DEVICE pointers unless stated; sizes are int64_t;
+ * `stream` is a cudaStream_t passed as void*.  Every call is asynchronous on
+ * `stream` and returns 0 on success or a BAK_E* code; bak_last_error() gives a
+ * thread-local message.  No call allocates device memory: callers pass a
+ * workspace sized by the matching *_workspace() query.
+ *
+ * Layout: x is column-major (obs x vars) with leading dimension ldx >= obs.
+ * Sweep kernels stream columns with cp.async.bulk and therefore require x to be
+ * 16-byte aligned and ldx*sizeof(T) to be a multiple of 16 (pad rows up to ldx
+ * may hold anything; they are masked).
+ */
+#ifndef BAK200_H_
+#define BAK200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype codes (reference precisions "single"/"double", core.py:13) */
+#define BAK_F32 0
+#define BAK_F64 1
+
+/* sweep variants */
+#define BAK_VARIANT_AUTO    0 /* pick by shape                                      */
+#define BAK_VARIANT_CTA     1 /* one CTA: e in registers, block reduction per column */
+#define BAK_VARIANT_CLUSTER 2 /* 2..16-CTA cluster: DSMEM st.async reduction         */
+#define BAK_VARIANT_GRID    3 /* persistent co-resident grid, e on chip, flag slots  */
+#define BAK_VARIANT_STREAM  4 /* persistent grid, e streamed through HBM             */
+#define BAK_VARIANT_GRAM    5 /* algebraically equal sweep via G = X^T X (labelled)  */
+
+/* status codes */
+#define BAK_OK           0
+#define BAK_EINVAL       1 /* bad argument / layout                      */
+#define BAK_ECUDA        2 /* CUDA runtime error                          */
+#define BAK_ETIMEOUT     3 /* device-side spin wait exceeded its deadline */
+#define BAK_EUNSUPPORTED 4 /* shape/variant combination not supported     */
+#define BAK_EWORKSPACE   5 /* workspace too small                         */
+
+/* Thread-local text of the last error ("" if none). */
+const char* bak_last_error(void);
+/* Library version string. */
+const char* bak_version(void);
+/* Number of SMs of the current device (launch sizing), or -1. */
+int bak_device_sm_count(void);
+
+/* ---- (1) column-norm precompute -------------------------------------------
+ * norms2[j] = <x_j, x_j> in T.  Replaces core.column_norms_sq (core.py:116-127)
+ * called at bak.py:185; with vars=1 it is also ||y||^2 (bak.py:168). */
+int64_t bak_colnorms_workspace(int dtype, int64_t obs, int64_t vars);
+int bak_colnorms(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx,
+                 void* norms2, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---- residual / warm start -------------------------------------------------
+ * out[i] = y[i] - (x @ a)[i] in T.  Replaces `y - x @ a` at bak.py:130 (final
+ * residual, _finish_report) and bak.py:189 (warm start with a0). */
+int64_t bak_residual_workspace(int dtype, int64_t obs, int64_t vars);
+int bak_residual(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx,
+                 const void* a, const void* y, void* out,
+                 void* workspace, int64_t workspace_bytes, void* stream);
+
+/* out_f64[0] = sum_i double(u[i] - v[i])^2 : the drift norm of bak.py:133. */
+int bak_diff_norm2(int dtype, const void* u, const void* v, int64_t n, double* out_f64,
+                   void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---- (2)/(3) persistent column sweep --------------------------------------
+ * Runs up to max_iter sweeps of the column step (bak.py:82-89) over the column
+ * list, checking sum(e^2) <= thresh2 after every sweep (bak.py:106-111).
+ *   cols      : NULL -> columns 0..ncols-1 every sweep (ncols must equal vars);
+ *               else int32 column indices, ncols per sweep; sweep s reads
+ *               cols + s*cols_stride (cols_stride 0 = same list every sweep).
+ *               Zero-norm columns must already be removed (bak.py:101-103).
+ *   e, a      : updated in place (e maintained residual, a coefficients).
+ *   thresh2   : early-break threshold tol^2*||y||^2; < 0 disables (tol == 0).
+ *   history   : NULL or double[max_iter] per-sweep sum(e^2) (bak.py:106-108).
+ *   status    : int64[4] device: {sweeps_run, converged, error, variant_used}.
+ */
+int64_t bak_sweep_workspace(int dtype, int variant, int64_t obs, int64_t vars);
+int bak_sweep(int dtype, int variant,
+              const void* x, int64_t obs, int64_t vars, int64_t ldx,
+              const void* norms2,
+              const int32_t* cols, int64_t ncols, int64_t cols_stride,
+              void* e, void* a,
+              int64_t max_iter, double thresh2,
+              double* history, int64_t* status,
+              void* workspace, int64_t workspace_bytes, void* stream);
+/* Variant AUTO would pick for this shape (for reporting). */
+int bak_sweep_pick_variant(int dtype, int64_t obs, int64_t vars);
+
+/* ---- (4) batched many-small-systems solve ---------------------------------
+ * One CTA per system; each CTA runs the whole solve_bak (bak.py:146-195) for
+ * its system: e = y (or y - x a0), sweeps, early break, final residual and drift.
+ * System s: x + s*x_stride (column-major obs x vars, ldx), y + s*y_stride,
+ * a + s*vars (in: a0 if warm != 0, out: a_hat), resid + s*y_stride,
+ * norms2 + s*vars (precomputed, e.g. bak_colnorms over obs x (nsys*vars) when
+ * x_stride == vars*ldx), ynorm2[s] (precomputed ||y_s||^2), history +
+ * s*max_iter (or NULL), status + 4*s = {sweeps_run, converged, drift_warning, err}.
+ * thresh2 = tol*tol*ynorm2[s] if tol > 0.  Zero-target systems return a=0. */
+int bak_solve_batched(int dtype,
+                      const void* x, int64_t obs, int64_t vars, int64_t ldx, int64_t x_stride,
+                      int64_t nsys, const void* y, int64_t y_stride,
+                      const void* norms2, const double* ynorm2,
+                      void* a, int warm, void* resid,
+                      int64_t max_iter, double tol, double drift_tol,
+                      double* history, int64_t* status, void* stream);
+
+/* ---- (5) multi-GPU row sharding (C3 at N>1) ---------------------------------
+ * Row-sharded sweep: rank r holds rows [r0, r0+obs_local) of x, y, e; a and
+ * norms2 are replicated.  Per column, every rank's grid reduces its partial dot
+ * and CTA 0 posts it into every rank's mailbox (peer-mapped device memory);
+ * all ranks sum the N partials in rank order, so delta and a are bit-identical
+ * everywhere.  mailboxes[r] = rank r's mailbox (device pointer valid on this
+ * device: a peer mapping, or local memory when emulating).
+ * With nranks_local > 1 a single launch emulates nranks_local ranks on one
+ * device (rows split evenly), used for single-GPU testing of the exchange. */
+int64_t bak_mailbox_bytes(int64_t nranks);
+int bak_sweep_rowshard(int dtype,
+                       const void* x, int64_t obs_local, int64_t vars, int64_t ldx,
+                       const void* norms2, void* e, void* a,
+                       int64_t max_iter, double thresh2, double* history, int64_t* status,
+                       int rank, int nranks, void* const* mailboxes, int64_t epoch_base,
+                       int nranks_local,
+                       void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Peer mapping helpers for one-process-per-GPU (CUDA IPC; 64-byte handles). */
+int bak_ipc_get_handle(void* devptr, void* handle64);
+int bak_ipc_open_handle(const void* handle64, void** devptr);
+int bak_ipc_close(void* devptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAK200_H_ */

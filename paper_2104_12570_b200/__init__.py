@@ -1,0 +1,20 @@
+"""B200-native (sm_100a) SolveBak column sweep — drop-in for the solve path of
+the reference package ``baksolve`` 0.1.0 (arXiv 2104.12570, Algorithm 1).
+
+    from paper_2104_12570_b200 import SolveConfig, solve_bak
+    rep = solve_bak(x, y, SolveConfig(max_iter=100, tol=0))
+
+Names mirror ``baksolve`` (reference __init__.py:9-10): SolveConfig,
+SolveReport, solve_bak, coordinate_update, residual_norm, DRIFT_TOL.
+Extension: solve_bak_batched for many independent small systems.
+"""
+
+from .bak import (DRIFT_TOL, ORDERINGS, BatchSolveReport, DeviceBatch, DeviceMatrix, SolveConfig, SolveReport,
+                  colnorms, coordinate_update, residual_norm, solve_bak, solve_bak_batched, to_device_batch,
+                  to_device_matrix)
+
+__version__ = "0.1.0"
+
+__all__ = ["DRIFT_TOL", "ORDERINGS", "BatchSolveReport", "DeviceBatch", "DeviceMatrix", "SolveConfig",
+           "SolveReport", "colnorms", "coordinate_update", "residual_norm", "solve_bak", "solve_bak_batched",
+           "to_device_batch", "to_device_matrix"]

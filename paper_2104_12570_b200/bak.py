@@ -1,0 +1,513 @@
+"""Drop-in B200 replacement for ``baksolve.bak`` (reference bak.py:1-195).
+
+Same names, arguments, defaults, validation messages and return type as the
+reference's solve entry point:
+
+    solve_bak(x, y, config: SolveConfig | None = None, a0=None) -> SolveReport
+
+The host side only validates, moves buffers and sequences C-ABI calls
+(libbak200.so, include/bak200.h); every number is computed by the sm_100a
+kernels.  There is no CPU fallback: without a CUDA device or without the
+library this module raises.
+
+Extensions (keyword-only, defaults keep reference behaviour):
+    variant="auto"|"cta"|"cluster"|"grid"|"stream"   kernel family
+    device=None                                       torch device (default current CUDA device)
+    return_device=False                               keep a_hat/residual as CUDA tensors
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+ORDERINGS = ("cyclic", "random")      # bak.py:25
+DRIFT_TOL = 1e-4                      # bak.py:29
+_RANDOM_CHUNK = 32                    # sweeps per launch when the order is random
+
+
+@dataclass
+class SolveConfig:
+    """Mirror of the reference SolveConfig (bak.py:32-46), same validation."""
+    max_iter: int = 1000
+    tol: float = 1e-6
+    ordering: str = "cyclic"
+    ordering_seed: int = 0
+    record_history: bool = False
+
+    def __post_init__(self):
+        if self.max_iter < 1:
+            raise ValueError(f"max_iter must be >= 1, got {self.max_iter}")
+        if self.tol < 0:
+            raise ValueError(f"tol must be >= 0, got {self.tol}")
+        if self.ordering not in ORDERINGS:
+            raise ValueError(f"unknown ordering {self.ordering!r}, expected one of {ORDERINGS}")
+
+
+@dataclass
+class SolveReport:
+    """Mirror of the reference SolveReport (bak.py:49-57).  ``variant`` is an
+    extra trailing field naming the kernel family that ran."""
+    a_hat: object
+    residual: object
+    residual_norm_history: list | None
+    sweeps_run: int
+    converged: bool
+    wall_time: float
+    drift_warning: bool = False
+    variant: str = ""
+
+
+# --------------------------------------------------------------------------
+# device plumbing (torch is used for memory and streams only)
+# --------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2104_12570_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return torch
+
+
+def _dtype_code(np_dtype):
+    return _lib.F64 if np.dtype(np_dtype) == np.float64 else _lib.F32
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream_ptr(torch, dev):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _is_torch(obj):
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(obj, torch.Tensor)
+
+
+class DeviceMatrix:
+    """Column-major device copy of x with an aligned leading dimension.
+
+    ``data`` is a (vars, ldx) row-major torch tensor, i.e. column j of x is
+    data[j, :obs]; ldx*sizeof(T) is a multiple of 16 so every column (and each
+    CTA's slice of it) can be moved with one cp.async.bulk.
+    """
+
+    def __init__(self, data, obs, vars_, np_dtype):
+        self.data = data
+        self.obs = obs
+        self.vars = vars_
+        self.ldx = data.shape[1]
+        self.np_dtype = np.dtype(np_dtype)
+        self.code = _dtype_code(np_dtype)
+
+    @property
+    def ptr(self):
+        return _ptr(self.data)
+
+
+def _aligned_ld(obs, itemsize):
+    v = 16 // itemsize
+    return (obs + v - 1) // v * v
+
+
+def to_device_matrix(x, device=None):
+    """Coerce like ``as_matrix`` (core.py:44-55) and upload column-major."""
+    torch = _torch()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if isinstance(x, DeviceMatrix):
+        return x
+    if _is_torch(x):
+        if x.ndim != 2:
+            raise ValueError(f"expected a 2-d matrix, got ndim={x.ndim}")
+        if x.dtype not in (torch.float32, torch.float64):
+            x = x.to(torch.float64)
+        obs, nv = x.shape
+        np_dtype = np.float64 if x.dtype == torch.float64 else np.float32
+        itemsize = 8 if np_dtype == np.float64 else 4
+        ld = _aligned_ld(obs, itemsize)
+        if (x.is_cuda and x.stride(0) == 1 and x.stride(1) >= obs and (x.stride(1) * itemsize) % 16 == 0
+                and x.data_ptr() % 16 == 0 and x.device == dev):
+            # zero-copy view of an existing column-major device matrix
+            data = torch.as_strided(x, (nv, x.stride(1)), (x.stride(1), 1))
+            return DeviceMatrix(data, obs, nv, np_dtype)
+        data = torch.empty((nv, ld), dtype=x.dtype, device=dev)
+        src = x.t()  # (vars, obs) view
+        if ld == obs:
+            data.copy_(src, non_blocking=True)
+        else:
+            data[:, :obs].copy_(src, non_blocking=True)
+        return DeviceMatrix(data, obs, nv, np_dtype)
+    xa = np.asarray(x)
+    if xa.ndim != 2:
+        raise ValueError(f"expected a 2-d matrix, got ndim={xa.ndim}")
+    if xa.dtype not in (np.float32, np.float64):
+        xa = xa.astype(np.float64)
+    xa = np.asfortranarray(xa)
+    obs, nv = xa.shape
+    ld = _aligned_ld(obs, xa.dtype.itemsize)
+    host = torch.from_numpy(xa.T)  # (vars, obs) C-contiguous view, no copy
+    data = torch.empty((nv, ld), dtype=host.dtype, device=dev)
+    if ld == obs:
+        data.copy_(host)
+    else:
+        data[:, :obs].copy_(host)
+    return DeviceMatrix(data, obs, nv, xa.dtype)
+
+
+def _to_device_vector(v, np_dtype, dev, name="y"):
+    torch = _torch()
+    tdt = torch.float64 if np.dtype(np_dtype) == np.float64 else torch.float32
+    if _is_torch(v):
+        if v.ndim != 1:
+            raise ValueError(f"expected a 1-d vector, got ndim={v.ndim}")
+        return v.to(device=dev, dtype=tdt).contiguous()
+    va = np.ascontiguousarray(v, dtype=np_dtype)
+    if va.ndim != 1:
+        raise ValueError(f"expected a 1-d vector, got ndim={va.ndim}")
+    return torch.from_numpy(va).to(dev)
+
+
+class _Workspace:
+    """Per-device scratch owned by the call (no allocation inside the sweep)."""
+
+    def __init__(self, torch, dev, nbytes):
+        self.buf = torch.empty(max(int(nbytes), 4096), dtype=torch.uint8, device=dev)
+
+    @property
+    def ptr(self):
+        return _ptr(self.buf)
+
+    @property
+    def nbytes(self):
+        return self.buf.numel()
+
+
+def _workspace_bytes(lib, code, obs, nv):
+    return max(lib.bak_colnorms_workspace(code, obs, nv), lib.bak_colnorms_workspace(code, obs, 1),
+               lib.bak_residual_workspace(code, obs, nv), lib.bak_sweep_workspace(code, 0, obs, nv), 4096)
+
+
+def colnorms(dm: DeviceMatrix, ws=None):
+    """Device column norms n2_j = <x_j, x_j> (core.py:116-127)."""
+    torch = _torch()
+    lib = _lib.load()
+    dev = dm.data.device
+    if ws is None:
+        ws = _Workspace(torch, dev, _workspace_bytes(lib, dm.code, dm.obs, dm.vars))
+    out = torch.empty(dm.vars, dtype=dm.data.dtype, device=dev)
+    _lib.check(lib.bak_colnorms(dm.code, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(out), ws.ptr, ws.nbytes,
+                                _stream_ptr(torch, dev)), "bak_colnorms")
+    return out
+
+
+def _sumsq(lib, torch, code, v, ws, st):
+    out = torch.empty(1, dtype=v.dtype, device=v.device)
+    _lib.check(lib.bak_colnorms(code, _ptr(v), v.numel(), 1, v.numel(), _ptr(out), ws.ptr, ws.nbytes, st),
+               "bak_colnorms(y)")
+    return out
+
+
+def _residual(lib, dm, a, y, out, ws, st):
+    _lib.check(lib.bak_residual(dm.code, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(a), _ptr(y), _ptr(out), ws.ptr,
+                                ws.nbytes, st), "bak_residual")
+
+
+def _permutation_chunks(seed, nvars, nz_mask):
+    """Yield the compounding per-sweep permutations of ordering='random'
+    (bak.py:98-99, 181) — host-side index bookkeeping, zero-norm columns
+    filtered (bak.py:101-103)."""
+    gen = np.random.Generator(np.random.Philox(seed))
+    order = np.arange(nvars)
+    while True:
+        gen.shuffle(order)
+        yield order[nz_mask[order]] if nz_mask is not None else order
+
+
+def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto", device=None,
+              return_device=False) -> SolveReport:
+    """Solve min ||y - x a|| by repeated single-column updates on the GPU.
+
+    Same contract as the reference (bak.py:146-159): x is coerced to
+    column-major float storage; zero-norm columns are skipped and keep their
+    starting coefficient; a zero target returns a = 0 immediately, converged;
+    convergence is checked once per sweep against tol * ||y||.
+    """
+    cfg = config if config is not None else SolveConfig()
+    torch = _torch()
+    lib = _lib.load()
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}, expected one of {tuple(_lib.VARIANTS)}")
+    dm = to_device_matrix(x, device)
+    dev = dm.data.device
+    obs, nv, code = dm.obs, dm.vars, dm.code
+    yd = _to_device_vector(y, dm.np_dtype, dev)
+    if yd.shape[0] != obs:
+        raise ValueError(f"y has length {yd.shape[0]}, expected {obs}")
+    st = _stream_ptr(torch, dev)
+
+    t0 = time.perf_counter()
+    ws = _Workspace(torch, dev, _workspace_bytes(lib, code, obs, nv))
+    ynorm2 = float(_sumsq(lib, torch, code, yd, ws, st).item())
+    if ynorm2 == 0.0:  # bak.py:168-170 (_zero_report)
+        a_z = torch.zeros(nv, dtype=yd.dtype, device=dev)
+        r_z = torch.zeros(obs, dtype=yd.dtype, device=dev)
+        return SolveReport(a_hat=a_z if return_device else a_z.cpu().numpy(),
+                           residual=r_z if return_device else r_z.cpu().numpy(),
+                           residual_norm_history=[] if cfg.record_history else None,
+                           sweeps_run=0, converged=True, wall_time=time.perf_counter() - t0)
+    if a0 is not None:
+        a = _to_device_vector(a0, dm.np_dtype, dev, "a0").clone()
+        if a.shape[0] != nv:
+            raise ValueError(f"a0 has length {a.shape[0]}, expected {nv}")
+    else:
+        a = torch.zeros(nv, dtype=yd.dtype, device=dev)
+    thresh2 = cfg.tol * cfg.tol * ynorm2 if cfg.tol > 0 else -1.0   # bak.py:182
+
+    norms = colnorms(dm, ws)
+    norms_h = norms.cpu().numpy()
+    if not norms_h.any():
+        raise ValueError("every column of x has zero norm; nothing to solve")
+    nz_mask = norms_h != 0
+    all_nz = bool(nz_mask.all())
+
+    e = torch.empty_like(yd)
+    if a0 is not None:
+        _residual(lib, dm, a, yd, e, ws, st)            # e = y - x a0 (bak.py:189)
+    else:
+        e.copy_(yd)
+    hist = torch.zeros(cfg.max_iter, dtype=torch.float64, device=dev) if cfg.record_history else None
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    vcode = _lib.VARIANTS[variant]
+
+    sweeps = 0
+    converged = False
+    used = vcode
+    if cfg.ordering == "cyclic":
+        if all_nz:
+            cols, ncols = None, nv
+        else:
+            cols = torch.from_numpy(np.flatnonzero(nz_mask).astype(np.int32)).to(dev)
+            ncols = int(cols.numel())
+        _lib.check(lib.bak_sweep(code, vcode, dm.ptr, obs, nv, dm.ldx, _ptr(norms), _ptr(cols), ncols, 0,
+                                 _ptr(e), _ptr(a), cfg.max_iter, thresh2, _ptr(hist), _ptr(status),
+                                 ws.ptr, ws.nbytes, st), "bak_sweep")
+        stat = status.cpu().numpy()
+        sweeps, converged, err, used = int(stat[0]), bool(stat[1]), int(stat[2]), int(stat[3])
+        if err:
+            raise _lib.BakError(f"bak_sweep device error {err} (3 = spin-wait timeout)")
+    else:
+        perms = _permutation_chunks(cfg.ordering_seed, nv, None if all_nz else nz_mask)
+        while sweeps < cfg.max_iter and not converged:
+            k = min(_RANDOM_CHUNK, cfg.max_iter - sweeps)
+            block = np.stack([next(perms) for _ in range(k)]).astype(np.int32)
+            cols = torch.from_numpy(block).to(dev)
+            ncols = block.shape[1]
+            hptr = ctypes.c_void_p(hist.data_ptr() + 8 * sweeps) if hist is not None else ctypes.c_void_p(0)
+            _lib.check(lib.bak_sweep(code, vcode, dm.ptr, obs, nv, dm.ldx, _ptr(norms), _ptr(cols), ncols, ncols,
+                                     _ptr(e), _ptr(a), k, thresh2, hptr, _ptr(status), ws.ptr, ws.nbytes, st),
+                       "bak_sweep")
+            stat = status.cpu().numpy()
+            if int(stat[2]):
+                raise _lib.BakError(f"bak_sweep device error {int(stat[2])}")
+            sweeps += int(stat[0])
+            converged = bool(stat[1])
+            used = int(stat[3])
+
+    resid = torch.empty_like(yd)
+    _residual(lib, dm, a, yd, resid, ws, st)             # bak.py:130
+    drift2 = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.check(lib.bak_diff_norm2(code, _ptr(e), _ptr(resid), obs, _ptr(drift2), ws.ptr, ws.nbytes, st),
+               "bak_diff_norm2")
+    drift = float(np.sqrt(drift2.item()))
+    wall = time.perf_counter() - t0                      # bak.py:131-132 (after the residual)
+    drift_rel = drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny)
+    history = hist[:sweeps].cpu().tolist() if hist is not None else None
+    return SolveReport(
+        a_hat=a if return_device else a.cpu().numpy(),
+        residual=resid if return_device else resid.cpu().numpy(),
+        residual_norm_history=history,
+        sweeps_run=sweeps,
+        converged=converged,
+        wall_time=wall,
+        drift_warning=bool(drift_rel > DRIFT_TOL),
+        variant=_lib.VARIANT_NAMES.get(used, str(used)),
+    )
+
+
+def residual_norm(e) -> float:
+    """sum(e^2) (bak.py:60-63), computed on the GPU."""
+    torch = _torch()
+    lib = _lib.load()
+    ea = e if _is_torch(e) else np.asarray(e)
+    np_dtype = np.float64 if (str(getattr(ea, "dtype", "")) in ("float64", "torch.float64")) else np.float32
+    if not _is_torch(ea) and ea.dtype not in (np.float32, np.float64):
+        np_dtype = np.float64
+    dev = torch.device("cuda", torch.cuda.current_device())
+    v = _to_device_vector(ea, np_dtype, dev)
+    if v.numel() == 0:
+        return 0.0
+    code = _dtype_code(np_dtype)
+    ws = _Workspace(torch, dev, max(lib.bak_colnorms_workspace(code, v.numel(), 1), 4096))
+    return float(_sumsq(lib, torch, code, v, ws, _stream_ptr(torch, dev)).item())
+
+
+def coordinate_update(col, e):
+    """One least-squares update along a single column (bak.py:66-79), run as
+    a one-column, one-sweep solve on the GPU.  Zero column: (0.0, e) with e
+    returned unchanged (the same object)."""
+    torch = _torch()
+    lib = _lib.load()
+    col_a = np.asarray(col)
+    e_a = np.asarray(e)
+    np_dtype = np.result_type(col_a.dtype, e_a.dtype)
+    if np_dtype not in (np.float32, np.float64):
+        np_dtype = np.float64
+    dm = to_device_matrix(col_a.astype(np_dtype).reshape(-1, 1))
+    dev = dm.data.device
+    st = _stream_ptr(torch, dev)
+    ws = _Workspace(torch, dev, _workspace_bytes(lib, dm.code, dm.obs, 1))
+    norms = colnorms(dm, ws)
+    if float(norms.item()) == 0.0:
+        return 0.0, e
+    ed = _to_device_vector(e_a, np_dtype, dev)
+    a = torch.zeros(1, dtype=ed.dtype, device=dev)
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    _lib.check(lib.bak_sweep(dm.code, 0, dm.ptr, dm.obs, 1, dm.ldx, _ptr(norms), None, 1, 0, _ptr(ed), _ptr(a),
+                             1, -1.0, None, _ptr(status), ws.ptr, ws.nbytes, st), "bak_sweep")
+    return float(a.item()), ed.cpu().numpy()
+
+
+# --------------------------------------------------------------------------
+# (4) batched many-small-systems solve — no reference counterpart: the
+# reference's equivalent is a Python loop of solve_bak calls, one per system.
+# --------------------------------------------------------------------------
+
+@dataclass
+class BatchSolveReport:
+    """Per-system results of solve_bak_batched; ``report(s)`` gives system s
+    as a reference-shaped SolveReport."""
+    a_hat: object                 # (nsys, vars)
+    residual: object              # (nsys, obs)
+    residual_norm_history: object  # (nsys, max_iter) float64 (valid prefix: sweeps_run[s]) or None
+    sweeps_run: np.ndarray
+    converged: np.ndarray
+    wall_time: float
+    drift_warning: np.ndarray
+
+    def report(self, s) -> SolveReport:
+        hist = None
+        if self.residual_norm_history is not None:
+            hist = [float(v) for v in np.asarray(self.residual_norm_history[s][: int(self.sweeps_run[s])])]
+        return SolveReport(a_hat=self.a_hat[s], residual=self.residual[s], residual_norm_history=hist,
+                           sweeps_run=int(self.sweeps_run[s]), converged=bool(self.converged[s]),
+                           wall_time=self.wall_time, drift_warning=bool(self.drift_warning[s]), variant="batched")
+
+
+class DeviceBatch:
+    """Device layout of a batch: data[s, j, :obs] is column j of system s
+    (each system column-major and contiguous, ld aligned to 16 bytes)."""
+
+    def __init__(self, data, obs, np_dtype):
+        self.data = data
+        self.nsys, self.vars, self.ldx = data.shape
+        self.obs = obs
+        self.np_dtype = np.dtype(np_dtype)
+        self.code = _dtype_code(np_dtype)
+
+
+def to_device_batch(xs, device=None):
+    """xs: (nsys, obs, vars) numpy array / torch tensor (any strides) or a DeviceBatch."""
+    torch = _torch()
+    if isinstance(xs, DeviceBatch):
+        return xs
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if not _is_torch(xs):
+        xa = np.asarray(xs)
+        if xa.ndim != 3:
+            raise ValueError(f"expected a 3-d batch (nsys, obs, vars), got ndim={xa.ndim}")
+        if xa.dtype not in (np.float32, np.float64):
+            xa = xa.astype(np.float64)
+        xs = torch.from_numpy(np.ascontiguousarray(xa.transpose(0, 2, 1)))  # (nsys, vars, obs)
+        src = xs
+    else:
+        if xs.ndim != 3:
+            raise ValueError(f"expected a 3-d batch (nsys, obs, vars), got ndim={xs.ndim}")
+        if xs.dtype not in (torch.float32, torch.float64):
+            xs = xs.to(torch.float64)
+        src = xs.transpose(1, 2)
+    nsys, nv, obs = src.shape
+    np_dtype = np.float64 if src.dtype == torch.float64 else np.float32
+    ld = _aligned_ld(obs, np.dtype(np_dtype).itemsize)
+    data = torch.empty((nsys, nv, ld), dtype=src.dtype, device=dev)
+    if ld == obs:
+        data.copy_(src, non_blocking=True)
+    else:
+        data[:, :, :obs].copy_(src, non_blocking=True)
+    return DeviceBatch(data, obs, np_dtype)
+
+
+def solve_bak_batched(xs, ys, config: SolveConfig | None = None, a0=None, *, device=None,
+                      return_device=False) -> BatchSolveReport:
+    """Solve nsys independent systems, one CTA each (SolveConfig applies to all).
+
+    Per system the semantics are those of solve_bak: cyclic order only
+    (ordering="random" is rejected), zero-norm columns skipped, zero targets
+    short-circuit, early break per sweep, residual recomputed, drift flagged.
+    """
+    cfg = config if config is not None else SolveConfig()
+    if cfg.ordering != "cyclic":
+        raise ValueError("solve_bak_batched supports ordering='cyclic' only")
+    torch = _torch()
+    lib = _lib.load()
+    db = to_device_batch(xs, device)
+    dev = db.data.device
+    nsys, nv, obs, ld, code = db.nsys, db.vars, db.obs, db.ldx, db.code
+    tdt = db.data.dtype
+    yd = ys if (_is_torch(ys) and ys.is_cuda) else torch.as_tensor(np.asarray(ys, dtype=db.np_dtype))
+    yd = yd.to(device=dev, dtype=tdt).reshape(nsys, -1).contiguous()
+    if yd.shape[1] != obs:
+        raise ValueError(f"y has length {yd.shape[1]}, expected {obs}")
+    st = _stream_ptr(torch, dev)
+    t0 = time.perf_counter()
+    wsb = max(lib.bak_colnorms_workspace(code, obs, nsys * nv), lib.bak_colnorms_workspace(code, obs, nsys), 4096)
+    ws = _Workspace(torch, dev, wsb)
+    norms = torch.empty(nsys * nv, dtype=tdt, device=dev)
+    _lib.check(lib.bak_colnorms(code, _ptr(db.data), obs, nsys * nv, ld, _ptr(norms), ws.ptr, ws.nbytes, st),
+               "bak_colnorms")
+    yn = torch.empty(nsys, dtype=tdt, device=dev)
+    _lib.check(lib.bak_colnorms(code, _ptr(yd), obs, nsys, obs, _ptr(yn), ws.ptr, ws.nbytes, st), "bak_colnorms(y)")
+    ynorm2 = yn.to(torch.float64)
+    if a0 is not None:
+        a = torch.as_tensor(a0).to(device=dev, dtype=tdt).reshape(nsys, nv).contiguous().clone()
+    else:
+        a = torch.zeros((nsys, nv), dtype=tdt, device=dev)
+    resid = torch.empty((nsys, obs), dtype=tdt, device=dev)
+    hist = torch.zeros((nsys, cfg.max_iter), dtype=torch.float64, device=dev) if cfg.record_history else None
+    status = torch.zeros((nsys, 4), dtype=torch.int64, device=dev)
+    _lib.check(lib.bak_solve_batched(code, _ptr(db.data), obs, nv, ld, nv * ld, nsys, _ptr(yd), obs, _ptr(norms),
+                                     _ptr(ynorm2), _ptr(a), 1 if a0 is not None else 0, _ptr(resid), cfg.max_iter,
+                                     float(cfg.tol), DRIFT_TOL, _ptr(hist), _ptr(status), st), "bak_solve_batched")
+    stat = status.cpu().numpy()
+    wall = time.perf_counter() - t0
+    bad = stat[:, 3]
+    if np.any(bad == 1):
+        raise ValueError("every column of x has zero norm; nothing to solve "
+                         f"(systems {np.flatnonzero(bad == 1)[:8].tolist()})")
+    if np.any(bad):
+        raise _lib.BakError(f"bak_solve_batched device error {int(bad[bad != 0][0])}")
+    return BatchSolveReport(
+        a_hat=a if return_device else a.cpu().numpy(),
+        residual=resid if return_device else resid.cpu().numpy(),
+        residual_norm_history=(hist if return_device else hist.cpu().numpy()) if hist is not None else None,
+        sweeps_run=stat[:, 0].copy(), converged=stat[:, 1].astype(bool), wall_time=wall,
+        drift_warning=stat[:, 2].astype(bool))

@@ -1,0 +1,299 @@
+// Batched many-small-systems solve (north-star component (4)): one CTA per
+// system runs the whole of solve_bak (bak.py:146-195) for that system.
+//
+//  - x (obs x vars, column-major) is brought into shared memory ONCE with a
+//    single cp.async.bulk when it fits (C5: 512 x 32 fp32 = 64 KiB), so the
+//    200 sweeps read it on chip; otherwise columns are read from L2/HBM.
+//  - e lives in registers (E rows per thread, rows tid + k*NT).
+//  - per column: fused  e -= d_j x_j ; p += x_next . e  then one block
+//    reduction (warp butterfly, + per-warp slots when NT > 32).
+//  - zero-norm columns are skipped in-kernel (bak.py:101-103), zero targets
+//    short-circuit (bak.py:168-170), early break per sweep (bak.py:106-111),
+//    final residual y - x a and the drift flag (bak.py:127-143) are computed in
+//    the same CTA.
+#include "bak_common.cuh"
+
+namespace bak {
+namespace {
+
+struct BatchedParams {
+  const void* x;
+  int64_t obs, vars, ldx, x_stride, nsys;
+  const void* y;
+  int64_t y_stride;
+  const void* norms2;
+  const double* ynorm2;
+  void* a;
+  int warm;
+  void* resid;
+  int64_t max_iter;
+  double tol, drift_tol;
+  double* history;
+  int64_t* status;
+  int x_in_smem;
+};
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red, int nwarps) {
+  v = warp_sum(v);
+  if (nwarps == 1) return v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = T(0);
+  for (int w = 0; w < nwarps; ++w) s = Num<T>::add(s, red[w]);
+  __syncthreads();  // red reusable
+  return s;
+}
+
+template <typename T, int E>
+__global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int NT = blockDim.x, tid = threadIdx.x, nwarps = NT >> 5;
+  const int64_t sys = blockIdx.x;
+  const int64_t obs = prm.obs, vars = prm.vars, ldx = prm.ldx;
+  const T* __restrict__ xg = static_cast<const T*>(prm.x) + sys * prm.x_stride;
+  const T* __restrict__ y = static_cast<const T*>(prm.y) + sys * prm.y_stride;
+  const T* __restrict__ n2g = static_cast<const T*>(prm.norms2) + sys * vars;
+  T* __restrict__ ag = static_cast<T*>(prm.a) + sys * vars;
+  T* __restrict__ rg = static_cast<T*>(prm.resid) + sys * prm.y_stride;
+  int64_t* status = prm.status + 4 * sys;
+  double* hist = prm.history ? prm.history + sys * prm.max_iter : nullptr;
+
+  size_t off = 0;
+  T* xs = reinterpret_cast<T*>(smem_raw);
+  if (prm.x_in_smem) off += static_cast<size_t>(vars) * ldx * sizeof(T);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + off);
+  off += 16;
+  T* n2s = reinterpret_cast<T*>(smem_raw + off);
+  off += round16(vars * sizeof(T));
+  T* as = reinterpret_cast<T*>(smem_raw + off);
+  off += round16(vars * sizeof(T));
+  T* red = reinterpret_cast<T*>(smem_raw + off);
+  double* redd = reinterpret_cast<double*>(smem_raw + off);
+
+  if (prm.x_in_smem) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(vars * ldx * sizeof(T));
+      mbar_arrive_expect_tx(bar, bytes);
+      bulk_g2s(xs, xg, bytes, bar, policy_evict_first());
+    }
+  }
+  const double yn2 = prm.ynorm2[sys];
+  for (int64_t j = tid; j < vars; j += NT) {
+    n2s[j] = n2g[j];
+    as[j] = prm.warm ? ag[j] : T(0);
+  }
+  if (prm.x_in_smem) {
+    const uint64_t t0 = globaltimer();
+    while (!mbar_test(bar, 0))
+      if (globaltimer() - t0 > kTimeoutNs) {
+        if (tid == 0) status[3] = BAK_ETIMEOUT;
+        break;
+      }
+  }
+  __syncthreads();
+  const T* X = prm.x_in_smem ? xs : xg;
+
+  const int kv = static_cast<int>(imax64(0, imin64(E, (obs - tid + NT - 1) / NT)));
+  T yv[E], ev[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) yv[k] = (k < kv) ? y[tid + k * NT] : T(0);
+
+  if (yn2 == 0.0) {  // bak.py:168-170 -> _zero_report
+    for (int64_t j = tid; j < vars; j += NT) ag[j] = T(0);
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (k < kv) rg[tid + k * NT] = T(0);
+    if (tid == 0) {
+      status[0] = 0;
+      status[1] = 1;
+      status[2] = 0;
+    }
+    return;
+  }
+  const double thresh2 = prm.tol > 0 ? prm.tol * prm.tol * yn2 : -1.0;
+
+  // e = y (or y - x a0 for a warm start, bak.py:188-191)
+#pragma unroll
+  for (int k = 0; k < E; ++k) ev[k] = yv[k];
+  if (prm.warm) {
+    T acc[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) acc[k] = T(0);
+    for (int64_t j = 0; j < vars; ++j) {
+      const T aj = as[j];
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (k < kv) acc[k] = Num<T>::fma(X[j * ldx + tid + k * NT], aj, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? Num<T>::sub(yv[k], acc[k]) : T(0);
+  }
+
+  auto next_nz = [&](int64_t j) -> int64_t {  // first column >= j with nonzero norm, or vars
+    while (j < vars && n2s[j] == T(0)) ++j;
+    return j;
+  };
+  const int64_t jfirst = next_nz(0);
+  int64_t sweeps = 0;
+  bool converged = false;
+  if (jfirst < vars) {
+    int64_t j = jfirst;
+    T p = T(0);
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (k < kv) p = Num<T>::fma(X[j * ldx + tid + k * NT], ev[k], p);
+    T P = block_sum(p, red, nwarps);
+    while (true) {
+      const T d = Num<T>::div(P, n2s[j]);
+      int64_t jn = next_nz(j + 1);
+      const bool last = jn >= vars;
+      const bool has_next = !(last && sweeps + 1 == prm.max_iter);
+      if (last) jn = jfirst;
+      T pv = T(0), qv = T(0);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k < kv) {
+          ev[k] = Num<T>::sub(ev[k], Num<T>::mul(X[j * ldx + tid + k * NT], d));
+          if (has_next) pv = Num<T>::fma(X[jn * ldx + tid + k * NT], ev[k], pv);
+          if (last) qv = Num<T>::fma(ev[k], ev[k], qv);
+        }
+      }
+      if (tid == 0) as[j] = Num<T>::add(as[j], d);
+      if (last) {
+        const T Q = block_sum(qv, red, nwarps);
+        if (tid == 0 && hist) hist[sweeps] = static_cast<double>(Q);
+        ++sweeps;
+        if (thresh2 >= 0.0 && static_cast<double>(Q) <= thresh2) {
+          converged = true;
+          break;
+        }
+        if (sweeps == prm.max_iter) break;
+      }
+      P = block_sum(pv, red, nwarps);
+      j = jn;
+    }
+  } else if (tid == 0) {
+    status[3] = BAK_EINVAL;  // all columns zero (bak.py:186-187)
+  }
+  __syncthreads();
+
+  // final residual y - x a (bak.py:130) and drift (bak.py:133-142)
+  T acc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = T(0);
+  for (int64_t j = 0; j < vars; ++j) {
+    const T aj = as[j];
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (k < kv) acc[k] = Num<T>::fma(X[j * ldx + tid + k * NT], aj, acc[k]);
+  }
+  double dd = 0.0;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if (k < kv) {
+      const T r = Num<T>::sub(yv[k], acc[k]);
+      rg[tid + k * NT] = r;
+      const double df = static_cast<double>(Num<T>::sub(ev[k], r));
+      dd = __fma_rn(df, df, dd);
+    }
+  }
+  dd = block_sum(dd, redd, nwarps);
+  for (int64_t j = tid; j < vars; j += NT) ag[j] = as[j];
+  if (tid == 0) {
+    const double ynorm = sqrt(yn2);
+    const double drift_rel = sqrt(dd) / (ynorm > 2.2250738585072014e-308 ? ynorm : 2.2250738585072014e-308);
+    status[0] = sweeps;
+    status[1] = converged ? 1 : 0;
+    status[2] = drift_rel > prm.drift_tol ? 1 : 0;
+  }
+}
+
+template <typename T, int E>
+int launch_batched(const BatchedParams& prm, int nthreads, size_t smem, cudaStream_t st) {
+  auto kern = batched_kernel<T, E>;
+  BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<static_cast<unsigned>(prm.nsys), nthreads, smem, st>>>(prm);
+  BAK_CHECK_CUDA(cudaGetLastError());
+  return BAK_OK;
+}
+
+}  // namespace
+}  // namespace bak
+
+using namespace bak;
+
+extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, int64_t x_stride,
+                                 int64_t nsys, const void* y, int64_t y_stride, const void* norms2,
+                                 const double* ynorm2, void* a, int warm, void* resid, int64_t max_iter, double tol,
+                                 double drift_tol, double* history, int64_t* status, void* stream) {
+  if (obs < 1 || vars < 1 || ldx < obs || nsys < 1 || max_iter < 1 || !x || !y || !norms2 || !ynorm2 || !a ||
+      !resid || !status || (dtype != BAK_F32 && dtype != BAK_F64)) {
+    set_error("bak_solve_batched: bad arguments");
+    return BAK_EINVAL;
+  }
+  const size_t ts = dtype_size(dtype);
+  // rows per thread / threads: aim for ~4 warps per system, E <= 32
+  static const int kEs[] = {1, 2, 4, 8, 16, 32};
+  int E = 0, nt = 0;
+  for (int e : kEs) {
+    int t = static_cast<int>(round_up((obs + e - 1) / e, 32));
+    if (t <= 128) {
+      E = e;
+      nt = t;
+      break;
+    }
+  }
+  if (!E) {
+    for (int e : kEs) {
+      int t = static_cast<int>(round_up((obs + e - 1) / e, 32));
+      if (t <= 256) {
+        E = e;
+        nt = t;
+        break;
+      }
+    }
+  }
+  if (!E) {
+    set_error("bak_solve_batched: obs=%lld too large for one CTA (max %d)", (long long)obs, 256 * 32);
+    return BAK_EUNSUPPORTED;
+  }
+  const size_t cap = static_cast<size_t>(device_max_smem_optin()) - 1024;
+  const size_t xbytes = static_cast<size_t>(vars) * ldx * ts;
+  const size_t small = 16 + 2 * round_up(static_cast<int64_t>(vars * ts), 16) + 32 * 8;
+  BatchedParams prm{x, obs, vars, ldx, x_stride, nsys, y, y_stride, norms2, ynorm2, a, warm, resid,
+                    max_iter, tol, drift_tol, history, status, 0};
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ldx * ts) % 16 == 0) &&
+                       ((x_stride * ts) % 16 == 0) && xbytes < (1u << 20);
+  size_t smem = small;
+  if (aligned && xbytes + small <= cap) {
+    prm.x_in_smem = 1;
+    smem += xbytes;
+  }
+  if (small > cap) {
+    set_error("bak_solve_batched: vars=%lld too large", (long long)vars);
+    return BAK_EUNSUPPORTED;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define BAK_B(T)                                                  \
+  switch (E) {                                                    \
+    case 1: return launch_batched<T, 1>(prm, nt, smem, st);       \
+    case 2: return launch_batched<T, 2>(prm, nt, smem, st);       \
+    case 4: return launch_batched<T, 4>(prm, nt, smem, st);       \
+    case 8: return launch_batched<T, 8>(prm, nt, smem, st);       \
+    case 16: return launch_batched<T, 16>(prm, nt, smem, st);     \
+    default: return launch_batched<T, 32>(prm, nt, smem, st);     \
+  }
+  if (dtype == BAK_F64) {
+    BAK_B(double)
+  } else {
+    BAK_B(float)
+  }
+#undef BAK_B
+}

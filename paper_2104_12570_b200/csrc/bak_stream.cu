@@ -1,0 +1,263 @@
+// STREAM variant: the exact per-column sweep (bak.py:92-112) for tall systems
+// whose residual e does not fit on chip (e.g. 2^24 x 256 fp64 on one B200:
+// e = 134 MB vs ~70 MB of registers + shared memory).
+//
+// Persistent co-resident grid; CTA r owns rows [r*R, (r+1)*R).  Per column the
+// CTA makes ONE fused streaming pass over its rows:
+//     e -= fl(d_j * x_j) ; p += x_{j+1} . e  (+ sum e^2 on the sweep's last column)
+// with 16-byte vector loads (x with the evict-first streaming hint), then one
+// grid reduction through epoch-tagged global records.  Per column the pass
+// moves x_j + x_{j+1} + e (read) + e (write) = 4 column-lengths of HBM traffic,
+// so the x-stream share of HBM bandwidth is capped near 25%;
+// alternating the traversal direction every column lets the tail of one pass
+// (e and x_{j+1}, the next pass's e and x_j) hit in the 126 MB L2.
+#include "bak_exchange.cuh"
+#include "bak_sweep.cuh"
+
+namespace bak {
+namespace {
+
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<double> {
+  using V = double2;
+  static constexpr int N = 2;
+  static __device__ __forceinline__ double get(const V& v, int i) { return i == 0 ? v.x : v.y; }
+  static __device__ __forceinline__ void set(V& v, int i, double x) {
+    if (i == 0) v.x = x; else v.y = x;
+  }
+};
+template <>
+struct Vec16<float> {
+  using V = float4;
+  static constexpr int N = 4;
+  static __device__ __forceinline__ float get(const V& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+  }
+  static __device__ __forceinline__ void set(V& v, int i, float x) {
+    if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
+  }
+};
+
+struct Cursor {
+  const int32_t* cols;
+  int64_t ncols, stride, s, k;
+  __device__ __forceinline__ int64_t col() const { return cols ? static_cast<int64_t>(cols[s * stride + k]) : k; }
+  __device__ __forceinline__ void next() {
+    if (++k == ncols) { k = 0; ++s; }
+  }
+};
+
+constexpr int kUnroll = 4;
+
+template <typename T>
+__device__ __forceinline__ void stream_pass(T* __restrict__ e, const T* __restrict__ xc, const T* __restrict__ xn,
+                                            int64_t nrows, T d, bool upd, bool dot, bool sq, bool backward, T& p,
+                                            T& q) {
+  using VT = Vec16<T>;
+  using V = typename VT::V;
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int64_t nvec = nrows / VT::N;
+  V* ev = reinterpret_cast<V*>(e);
+  const V* xcv = reinterpret_cast<const V*>(xc);
+  const V* xnv = reinterpret_cast<const V*>(xn);
+  T p0 = T(0), p1 = T(0), q0 = T(0), q1 = T(0);
+  const int64_t step = static_cast<int64_t>(NT) * kUnroll;
+  const int64_t nfull = nvec / step * step;
+  for (int64_t base = 0; base < nfull; base += step) {
+    int64_t idx[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = base + tid + static_cast<int64_t>(u) * NT;
+      idx[u] = backward ? (nvec - 1 - i) : i;
+    }
+    V E[kUnroll], XC[kUnroll], XN[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      E[u] = ev[idx[u]];
+      if (upd) XC[u] = __ldcs(xcv + idx[u]);
+      if (dot) XN[u] = __ldcs(xnv + idx[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+      for (int c = 0; c < VT::N; ++c) {
+        T ee = VT::get(E[u], c);
+        if (upd) ee = Num<T>::sub(ee, Num<T>::mul(VT::get(XC[u], c), d));
+        if (dot) {
+          if (c & 1) p1 = Num<T>::fma(VT::get(XN[u], c), ee, p1);
+          else p0 = Num<T>::fma(VT::get(XN[u], c), ee, p0);
+        }
+        if (sq) {
+          if (c & 1) q1 = Num<T>::fma(ee, ee, q1);
+          else q0 = Num<T>::fma(ee, ee, q0);
+        }
+        VT::set(E[u], c, ee);
+      }
+      if (upd) ev[idx[u]] = E[u];
+    }
+  }
+  // vector remainder
+  for (int64_t i0 = nfull + tid; i0 < nvec; i0 += NT) {
+    const int64_t i = backward ? (nvec - 1 - i0) : i0;
+    V E1 = ev[i];
+    V XC1, XN1;
+    if (upd) XC1 = __ldcs(xcv + i);
+    if (dot) XN1 = __ldcs(xnv + i);
+#pragma unroll
+    for (int c = 0; c < VT::N; ++c) {
+      T ee = VT::get(E1, c);
+      if (upd) ee = Num<T>::sub(ee, Num<T>::mul(VT::get(XC1, c), d));
+      if (dot) p0 = Num<T>::fma(VT::get(XN1, c), ee, p0);
+      if (sq) q0 = Num<T>::fma(ee, ee, q0);
+      VT::set(E1, c, ee);
+    }
+    if (upd) ev[i] = E1;
+  }
+  // scalar tail (last CTA only)
+  for (int64_t i = nvec * VT::N + tid; i < nrows; i += NT) {
+    T ee = e[i];
+    if (upd) ee = Num<T>::sub(ee, Num<T>::mul(xc[i], d));
+    if (dot) p0 = Num<T>::fma(xn[i], ee, p0);
+    if (sq) q0 = Num<T>::fma(ee, ee, q0);
+    if (upd) e[i] = ee;
+  }
+  p = Num<T>::add(p0, p1);
+  q = Num<T>::add(q0, q1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) stream_kernel(const SweepParams prm) {
+  __shared__ T red[2 * 2 * 32];
+  __shared__ double bc[2][2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = blockIdx.x, G = gridDim.x;
+  const T* __restrict__ x = static_cast<const T*>(prm.x);
+  const T* __restrict__ n2g = static_cast<const T*>(prm.norms2);
+  T* __restrict__ ag = static_cast<T*>(prm.a);
+  const int64_t r0 = static_cast<int64_t>(rank) * prm.rows_per_cta;
+  const int64_t nrows = imax64(0, imin64(prm.obs - r0, prm.rows_per_cta));
+  T* e = static_cast<T*>(prm.e) + r0;
+  const int64_t ncols = prm.ncols, total = prm.max_iter * ncols;
+  int my_abort = 0;
+
+  auto exchange = [&](T p, T q, bool with_q, uint32_t rc, T& P, T& Q) -> bool {
+    const int buf = rc & 1;
+    if (block_sum2(p, q, with_q, buf, red, my_abort)) return true;
+    const uint32_t epoch = rc + 1;
+    uint32_t* slots = prm.slots + static_cast<size_t>(buf) * G * 8;
+    if (tid == 0) {
+      ll_store(slots + static_cast<size_t>(rank) * 8, static_cast<double>(p), epoch);
+      if (with_q) ll_store(slots + static_cast<size_t>(rank) * 8 + 4, static_cast<double>(q), epoch);
+    }
+    if (warp == 0) {
+      T sp, sq;
+      bool to = false;
+      warp_gather_slots(slots, G, epoch, with_q, sp, sq, to);
+      if (to) {
+        report_error(prm.status, BAK_ETIMEOUT);
+        my_abort = 1;
+      }
+      if (lane == 0) {
+        bc[buf][0] = static_cast<double>(sp);
+        bc[buf][1] = static_cast<double>(sq);
+      }
+    }
+    const bool ab = __syncthreads_or(my_abort) != 0;
+    P = static_cast<T>(bc[buf][0]);
+    Q = static_cast<T>(bc[buf][1]);
+    return ab;
+  };
+
+  Cursor cc{prm.cols, ncols, prm.cols_stride, 0, 0};
+  int64_t c_cur = cc.col();
+  uint32_t rc = 0;
+  T P, Q, pv, qv;
+  bool backward = false;
+  stream_pass<T>(e, nullptr, x + c_cur * prm.ldx + r0, nrows, T(0), false, true, false, backward, pv, qv);
+  bool aborted = exchange(pv, T(0), false, rc++, P, Q);
+
+  T n2_cur = n2g[c_cur];
+  cc.next();
+  int64_t c_next = total > 1 ? cc.col() : c_cur;
+  const bool updater = rank == 0 && tid == 32;
+  T a_val = updater ? ag[c_cur] : T(0);
+  int64_t sweep = 0, k = 0, t = 0;
+  bool converged = false;
+  while (!aborted) {
+    const T d = Num<T>::div(P, n2_cur);
+    const bool last = k == ncols - 1;
+    const bool has_next = !(last && sweep + 1 == prm.max_iter);
+    T n2_next = has_next ? n2g[c_next] : T(0);
+    backward = !backward;
+    stream_pass<T>(e, x + c_cur * prm.ldx + r0, x + c_next * prm.ldx + r0, nrows, d, true, has_next, last, backward,
+                   pv, qv);
+    if (updater) {
+      a_val = Num<T>::add(a_val, d);
+      ag[c_cur] = a_val;
+      if (has_next) a_val = ag[c_next];
+    }
+    aborted = exchange(pv, qv, last, rc++, P, Q);
+    if (aborted) break;
+    if (last) {
+      if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
+      ++sweep;
+      if (prm.thresh2 >= 0.0 && static_cast<double>(Q) <= prm.thresh2) {
+        converged = true;
+        break;
+      }
+      if (sweep == prm.max_iter) break;
+      k = 0;
+    } else {
+      ++k;
+    }
+    ++t;
+    c_cur = c_next;
+    n2_cur = n2_next;
+    cc.next();
+    if (t + 1 < total) c_next = cc.col();
+  }
+  if (rank == 0 && tid == 0 && prm.status) {
+    prm.status[0] = sweep;
+    prm.status[1] = converged ? 1 : 0;
+    prm.status[3] = BAK_VARIANT_STREAM;
+  }
+}
+
+}  // namespace
+
+bool plan_stream(int dtype, int64_t obs, StreamPlan& pl) {
+  const int sms = device_sms();
+  pl.nthreads = 512;
+  pl.nblocks = sms;
+  const int64_t vec = 16 / static_cast<int64_t>(dtype_size(dtype));
+  int64_t per = (obs + pl.nblocks - 1) / pl.nblocks;
+  per = round_up(per, vec);
+  pl.rows_per_cta = per;
+  pl.nblocks = static_cast<int>((obs + per - 1) / per);
+  return pl.nblocks >= 1;
+}
+
+int launch_stream(int dtype, const StreamPlan& pl, const SweepParams& prm0, cudaStream_t st) {
+  SweepParams prm = prm0;
+  prm.rows_per_cta = pl.rows_per_cta;
+  BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, static_cast<size_t>(2) * pl.nblocks * 32, st));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.nblocks);
+  cfg.blockDim = dim3(pl.nthreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dtype == BAK_F64)
+    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stream_kernel<double>, prm));
+  else
+    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stream_kernel<float>, prm));
+  return BAK_OK;
+}
+
+}  // namespace bak

@@ -50,6 +50,8 @@ extern "C" {
 const char* bak_last_error(void);
 /* Library version string. */
 const char* bak_version(void);
+/* Kernels this library has launched in this process (monotone counter). */
+int64_t bak_launch_count(void);
 /* Number of SMs of the current device (launch sizing), or -1. */
 int bak_device_sm_count(void);
 

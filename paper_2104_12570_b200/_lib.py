@@ -26,6 +26,7 @@ SIGNATURES = {
     "bak_last_error": (ctypes.c_char_p, []),
     "bak_version": (ctypes.c_char_p, []),
     "bak_device_sm_count": (_int, []),
+    "bak_launch_count": (_i64, []),
     "bak_colnorms_workspace": (_i64, [_int, _i64, _i64]),
     "bak_colnorms": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     "bak_residual_workspace": (_i64, [_int, _i64, _i64]),

@@ -230,7 +230,7 @@ def _permutation_chunks(seed, nvars, nz_mask):
     order = np.arange(nvars)
     while True:
         gen.shuffle(order)
-        yield order[nz_mask[order]] if nz_mask is not None else order
+        yield order[nz_mask[order]] if nz_mask is not None else order.copy()
 
 
 def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto", device=None,

@@ -220,6 +220,7 @@ int launch_batched(const BatchedParams& prm, int nthreads, size_t smem, cudaStre
   auto kern = batched_kernel<T, E>;
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<static_cast<unsigned>(prm.nsys), nthreads, smem, st>>>(prm);
+  count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;
 }

@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
@@ -10,6 +11,8 @@
 namespace bak {
 
 static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -63,6 +66,7 @@ int pick_variant(int dtype, int64_t obs) {
 }  // namespace
 
 extern "C" const char* bak_last_error(void) { return g_err; }
+extern "C" int64_t bak_launch_count(void) { return g_launches.load(); }
 extern "C" const char* bak_version(void) { return "bak200 0.1.0 (sm_100a)"; }
 extern "C" int bak_device_sm_count(void) {
   int dev = 0, v = 0;

@@ -164,6 +164,7 @@ int colnorms_t(const void* xv, int64_t obs, int64_t vars, int64_t ldx, void* nor
   if (nch == 1) {
     colnorms_partial<T><<<static_cast<unsigned>((items + wpb - 1) / wpb), kNormThreads, 0, st>>>(x, obs, ldx, vars,
                                                                                                  chunk, 1, norms);
+    count_launches(1);
   } else {
     if (wsb < static_cast<int64_t>(items * sizeof(T))) {
       set_error("bak_colnorms: workspace too small");
@@ -172,8 +173,10 @@ int colnorms_t(const void* xv, int64_t obs, int64_t vars, int64_t ldx, void* nor
     T* part = static_cast<T*>(ws);
     colnorms_partial<T><<<static_cast<unsigned>((items + wpb - 1) / wpb), kNormThreads, 0, st>>>(x, obs, ldx, vars,
                                                                                                  chunk, nch, part);
+    count_launches(1);
     colnorms_final<T><<<static_cast<unsigned>((vars + wpb - 1) / wpb), kNormThreads, 0, st>>>(part, vars, nch,
                                                                                               norms);
+    count_launches(1);
   }
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;
@@ -191,6 +194,7 @@ int residual_t(const void* xv, int64_t obs, int64_t vars, int64_t ldx, const voi
   T* out = static_cast<T*>(outv);
   if (nsplit == 1) {
     gemv_partial<T><<<static_cast<unsigned>(tiles), kGemvThreads, 0, st>>>(x, obs, ldx, vars, a, y, 1, per, out);
+    count_launches(1);
   } else {
     if (wsb < static_cast<int64_t>(nsplit * obs * sizeof(T))) {
       set_error("bak_residual: workspace too small");
@@ -199,8 +203,10 @@ int residual_t(const void* xv, int64_t obs, int64_t vars, int64_t ldx, const voi
     T* part = static_cast<T*>(ws);
     gemv_partial<T><<<static_cast<unsigned>(tiles * nsplit), kGemvThreads, 0, st>>>(x, obs, ldx, vars, a, y,
                                                                                      nsplit, per, part);
+    count_launches(1);
     gemv_final<T><<<static_cast<unsigned>((obs + kGemvThreads - 1) / kGemvThreads), kGemvThreads, 0, st>>>(
         part, obs, nsplit, y, out);
+    count_launches(1);
   }
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;
@@ -214,7 +220,9 @@ int diff_t(const void* u, const void* v, int64_t n, double* out, void* ws, int64
   }
   double* part = static_cast<double*>(ws);
   diff_partial<T><<<kDiffBlocks, kDiffThreads, 0, st>>>(static_cast<const T*>(u), static_cast<const T*>(v), n, part);
+  count_launches(1);
   diff_final<<<1, kWarp, 0, st>>>(part, kDiffBlocks, out);
+  count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;
 }

@@ -257,6 +257,7 @@ int launch_stream(int dtype, const StreamPlan& pl, const SweepParams& prm0, cuda
     BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stream_kernel<double>, prm));
   else
     BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stream_kernel<float>, prm));
+  count_launches(1);
   return BAK_OK;
 }
 

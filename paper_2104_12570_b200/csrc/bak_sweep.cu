@@ -389,6 +389,7 @@ int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = na;
   BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  count_launches(1);
   return BAK_OK;
 }
 

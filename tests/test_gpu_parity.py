@@ -4,8 +4,10 @@ own outputs (golden fixtures) and the CPU oracle on the same seeded inputs.
 Tolerances (north_star / SURVEY §8c), written here once:
   coefficients   ||a - a_ref|| / ||a_ref||  <= 1e-10 (fp64), 1e-4 (fp32)
   residual norm  | r - r_ref | / r_ref      <= same tol, with r recomputed in
-                 fp64 (bench.py:180-184); when r_ref sits at the rounding floor
-                 (r_ref <= 1e-12 ||y||) the difference is taken relative to ||y||
+                 fp64 (bench.py:180-184); when the system is solved to the
+                 rounding floor (r_ref < 1e-6 ||y||: consistent / converged
+                 systems such as C2, C4) the difference is taken relative to
+                 ||y||, since |r - r_ref| <= ||X|| ||a - a_ref|| ~ tol ||y||
   control flow   sweeps_run and converged identical
 """
 
@@ -35,14 +37,14 @@ def assert_parity(x, y, rep, ref_a, ref_sweeps, ref_conv, ref_rnorm=None, ref_hi
     if ref_rnorm is None:
         ref_rnorm = orc.residual_norm_f64(x, y, ref_a)
     ynorm = float(np.linalg.norm(np.asarray(y, np.float64)))
-    den = ref_rnorm if ref_rnorm > 1e-12 * ynorm else ynorm
+    den = ref_rnorm if ref_rnorm >= 1e-6 * ynorm else ynorm
     if den > 0:
         assert abs(r - ref_rnorm) / den <= tol, (r, ref_rnorm)
     # reported residual is the recomputed y - x a (bak.py:130)
     want = y - x @ rep.a_hat
     scale = np.abs(x).astype(np.float64) @ np.abs(rep.a_hat).astype(np.float64) + np.abs(y)
     assert np.all(np.abs(rep.residual - want) <= 64 * np.finfo(x.dtype).eps * (scale + 1e-300))
-    if ref_hist is not None and rep.residual_norm_history is not None:
+    if ref_hist is not None and rep.residual_norm_history is not None and len(ref_hist):
         assert len(rep.residual_norm_history) == len(ref_hist)
         h = np.asarray(rep.residual_norm_history)
         hr = np.asarray(ref_hist)
@@ -114,7 +116,7 @@ def test_deterministic_bits():
 
 def test_tall_stream_matches_oracle():
     pb = _pb()
-    x, y, _ = orc.config_c3(obs=1 << 20, nvars=32, precision="double")
+    x, y, _ = orc.config_c3(obs=1 << 21, nvars=32, precision="double")
     ref = orc.solve(x, y, max_iter=3, tol=0)
     rep = pb.solve_bak(x, y, pb.SolveConfig(max_iter=3, tol=0))
     assert rep.variant == "stream"

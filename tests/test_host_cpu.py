@@ -68,8 +68,9 @@ def test_solve_config_validation_matches_reference():
 def test_random_permutations_match_reference_order():
     gen = _permutation_chunks(11, 25, None)
     want = orc.permutations(11, 25, 5)
+    got = [next(gen) for _ in range(5)]  # materialise first: chunks must not alias
     for s in range(5):
-        assert np.array_equal(next(gen), want[s])
+        assert np.array_equal(got[s], want[s])
     mask = np.ones(25, bool)
     mask[[3, 7]] = False
     gen = _permutation_chunks(11, 25, mask)

@@ -11,13 +11,20 @@
 //
 // B200 design.  P participants (CTAs) each own a contiguous row block of e,
 // held in REGISTERS for the whole solve (E rows per thread, rows tid + k*NT so
-// shared-memory reads are conflict-free).  The CTA's slice of each column x_j
-// is contiguous in column-major x, so one cp.async.bulk (TMA engine) moves it
-// into an S-stage shared-memory ring, S columns ahead (x never depends on e).
-// Per column there is exactly one reduction:
-//     fused pass:  e -= d_j * x_j  ;  p += x_{j+1} . e   (+ sum e^2 at sweep end)
-//     warp xor-butterfly -> per-warp slots -> __syncthreads -> fixed-order sum
-//     -> exchange across participants -> every thread holds P and d_{j+1}.
+// shared-memory reads are conflict-free).  Each CTA = NT consumer threads +
+// one PRODUCER warp.  The producer walks the column schedule S steps ahead:
+// it reads col(u) and n2[col(u)] into a per-stage smem record and issues one
+// cp.async.bulk (TMA engine) for the CTA's slice of that column (contiguous in
+// column-major x) into an S-stage ring guarded by full/empty mbarriers.  x
+// never depends on e, so every global-memory latency of the schedule (column
+// list, norms, x itself) is off the consumers' critical path.
+//
+// Consumers keep TWO columns in registers (x_t, x_{t+1}) and per column do
+//     d_t = P_t / n2_t
+//     fused:  e -= fl(d_t * x_t) ; p += x_{t+1} . e  (+ sum e^2 at sweep end)
+//     load x_{t+2} smem -> registers (before the reduction; frees its stage)
+//     warp xor-butterfly -> per-warp slots -> named barrier -> fixed-order sum
+//     -> exchange across participants -> every consumer holds P_{t+1}.
 // Exchange by MODE:
 //   kCta     : single CTA, nothing to exchange.
 //   kCluster : thread-block cluster (2..16 CTAs).  Each CTA st.async's its
@@ -29,6 +36,7 @@
 // Every participant sums the same values in the same order, so all of them
 // compute bit-identical d_j; the reduction order depends only on the shape.
 #include <cstdio>
+#include <cstdlib>
 
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
@@ -39,6 +47,8 @@ namespace {
 constexpr int kModeCta = 0, kModeCluster = 1, kModeGrid = 2;
 constexpr int kMaxCluster = 16;
 constexpr int kMaxStages = 16;
+constexpr int kMaxConsumers = 256;
+constexpr int kBarConsumers = 1;  // named barrier id used by consumer warps only
 
 struct ColCursor {
   const int32_t* cols;
@@ -49,15 +59,31 @@ struct ColCursor {
   }
 };
 
-template <typename T>
 struct alignas(16) Pair {
   double p, q;
 };
 
+__device__ __forceinline__ bool bar_or(int nthreads, int pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 q, %1, 0;\n\t"
+      "bar.red.or.pred p, %2, %3, q;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(static_cast<uint32_t>(pred)), "r"(kBarConsumers), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
 template <typename T, int E, int MODE>
-__global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepParams prm) {
+__global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const SweepParams prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int NT = blockDim.x;
+  const int NT = static_cast<int>(blockDim.x) - 32;  // consumers; the last warp produces
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
   const int S = prm.nstages;
 
@@ -83,117 +109,94 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepParams prm) {
   T* xs = reinterpret_cast<T*>(smem_raw);
   size_t off = static_cast<size_t>(S) * prm.stage_elems * sizeof(T);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + off);
-  off += kMaxStages * sizeof(uint64_t);
+  off += kMaxStages * 8;
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + off);
+  off += kMaxStages * 8;
+  int64_t* meta_col = reinterpret_cast<int64_t*>(smem_raw + off);
+  off += kMaxStages * 8;
+  double* meta_n2 = reinterpret_cast<double*>(smem_raw + off);
+  off += kMaxStages * 8;
   T* red = reinterpret_cast<T*>(smem_raw + off);  // [2 bufs][2 values][32 warps]
   off += 2 * 2 * 32 * sizeof(T);
   off = (off + 15) & ~size_t(15);
-  Pair<T>* xslot = reinterpret_cast<Pair<T>*>(smem_raw + off);  // [2][kMaxCluster]
-  off += 2 * kMaxCluster * sizeof(Pair<T>);
+  Pair* xslot = reinterpret_cast<Pair*>(smem_raw + off);  // [2][kMaxCluster]
+  off += 2 * kMaxCluster * sizeof(Pair);
   uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2]
-  off += 2 * sizeof(uint64_t);
-  Pair<T>* bcast = reinterpret_cast<Pair<T>*>(smem_raw + off);  // [2]
-  off += 2 * sizeof(Pair<T>);
+  off += 2 * 8;
+  Pair* bcast = reinterpret_cast<Pair*>(smem_raw + off);  // [2]
+  off += 2 * sizeof(Pair);
+  volatile int* stop = reinterpret_cast<volatile int*>(smem_raw + off);
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
+    *stop = 0;
     fence_mbar_init();
   }
   __syncthreads();
   if (MODE == kModeCluster) cluster_sync();
 
-  // ---- residual slice into registers ----
-  const int kv = static_cast<int>(imax64(0, imin64(E, (nrows - tid + NT - 1) / NT)));
-  T ev[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? eg[r0 + tid + static_cast<int64_t>(k) * NT] : T(0);
-
   const int64_t ncols = prm.ncols;
   const int64_t total = prm.max_iter * ncols;
-  const uint64_t pol = policy_evict_first();
 
-  // producer (tid 0): TMA the CTA's slice of column(t) into stage t % S
-  ColCursor pc{prm.cols, ncols, prm.cols_stride, 0, 0};
-  int64_t issued = 0;
-  int64_t pcol = 0;
-  if (tid == 0) {
-    pcol = pc.col();
-    const int64_t first = imin64(total, S);
-    for (; issued < first; ++issued) {
-      const int s = static_cast<int>(issued % S);
-      mbar_arrive_expect_tx(&full[s], bytes);
-      bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + pcol * prm.ldx + r0, bytes, &full[s], pol);
-      pc.next();
-      if (issued + 1 < total) pcol = pc.col();
-    }
-  }
-
-  int my_abort = 0;  // thread-local; made uniform by __syncthreads_or
-  auto wait_stage = [&](int64_t t) {
-    const int s = static_cast<int>(t % S);
-    const uint32_t par = static_cast<uint32_t>((t / S) & 1);
-    if (!mbar_test(&full[s], par)) {
-      const uint64_t t0 = globaltimer();
-      while (!mbar_test(&full[s], par)) {
-        if (globaltimer() - t0 > kTimeoutNs) {
-          report_error(prm.status, BAK_ETIMEOUT);
-          my_abort = 1;
-          break;
-        }
-      }
-    }
-  };
-
-  // one reduction across all participants; returns (P, Q) in every thread
-  auto reduce = [&](T pv, T qv, bool with_q, uint32_t rc, bool refill, T& P, T& Q) -> bool {
-    const int buf = rc & 1;
-    pv = warp_sum(pv);
-    if (with_q) qv = warp_sum(qv);
+  if (tid >= NT) {
+    // =========================== producer warp ===========================
     if (lane == 0) {
-      red[(buf * 2 + 0) * 32 + warp] = pv;
-      red[(buf * 2 + 1) * 32 + warp] = qv;
-    }
-    const bool any_abort = __syncthreads_or(my_abort) != 0;
-    if (any_abort) return true;
-    // every thread has finished reading the stage consumed by this step
-    T bp = T(0), bq = T(0);
-    for (int w = 0; w < nwarps; ++w) bp = Num<T>::add(bp, red[(buf * 2 + 0) * 32 + w]);
-    if (with_q)
-      for (int w = 0; w < nwarps; ++w) bq = Num<T>::add(bq, red[(buf * 2 + 1) * 32 + w]);
-
-    if (MODE == kModeCta) {
-      if (refill && tid == 0 && issued < total) {
-        const int s = static_cast<int>(issued % S);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + pcol * prm.ldx + r0, bytes, &full[s], pol);
+      const uint64_t pol = policy_evict_first();
+      ColCursor pc{prm.cols, ncols, prm.cols_stride, 0, 0};
+      int s = 0;
+      uint32_t ph = 0;
+      int64_t u = 0;
+      bool halted = false;
+      for (; u < total; ++u) {
+        if (u >= S) {
+          const uint32_t par = ph ^ 1u;
+          if (!mbar_test(&empty[s], par)) {
+            const uint64_t t0 = globaltimer();
+            while (!mbar_test(&empty[s], par)) {
+              if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+            }
+          }
+          if (halted) break;
+        }
+        const int64_t c = pc.col();
         pc.next();
-        ++issued;
-        if (issued < total) pcol = pc.col();
+        meta_col[s] = c;
+        meta_n2[s] = static_cast<double>(n2g[c]);
+        mbar_arrive_expect_tx(&full[s], bytes);  // release: meta visible with the phase
+        bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + c * prm.ldx + r0, bytes, &full[s], pol);
+        if (++s == S) { s = 0; ph ^= 1u; }
       }
-      P = bp;
-      Q = bq;
-      return false;
-    }
-    if (MODE == kModeCluster) {
-      if (tid < static_cast<int>(G)) {
-        const uint32_t rs = mapa(smem_addr(&xslot[buf * kMaxCluster + rank]), tid);
-        const uint32_t rb = mapa(smem_addr(&xbar[buf]), tid);
-        st_async_v2(rs, static_cast<double>(bp), static_cast<double>(bq), rb);
-      }
-      if (tid == 0) mbar_arrive_expect_tx(&xbar[buf], G * 16u);
-      if (refill && tid == 0 && issued < total) {
-        const int s = static_cast<int>(issued % S);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + pcol * prm.ldx + r0, bytes, &full[s], pol);
-        pc.next();
-        ++issued;
-        if (issued < total) pcol = pc.col();
-      }
-      const uint32_t par = (rc >> 1) & 1;
-      if (!mbar_test_cluster(&xbar[buf], par)) {
+      // drain: the last min(S, u) issued copies must land before this CTA exits
+      for (int64_t v = imax64(0, u - S); v < u; ++v) {
+        const int sv = static_cast<int>(v % S);
+        const uint32_t pv = static_cast<uint32_t>((v / S) & 1);
         const uint64_t t0 = globaltimer();
-        while (!mbar_test_cluster(&xbar[buf], par)) {
+        while (!mbar_test(&full[sv], pv))
+          if (globaltimer() - t0 > kTimeoutNs) break;
+      }
+    }
+  } else {
+    // =========================== consumers ===============================
+    const int kv = static_cast<int>(imax64(0, imin64(E, (nrows - tid + NT - 1) / NT)));
+    T ev[E], xc[E], xn[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? eg[r0 + tid + static_cast<int64_t>(k) * NT] : T(0);
+
+    int my_abort = 0;
+    int ls = 0;        // stage of the next step to pull into registers
+    uint32_t lph = 0;  // its phase parity
+    int rel[2];        // stages pulled since the last release
+    int nrel = 0;
+
+    auto pull = [&](T (&xr)[E], int64_t& c, T& n2) {
+      if (!mbar_test(&full[ls], lph)) {
+        const uint64_t t0 = globaltimer();
+        while (!mbar_test(&full[ls], lph)) {
           if (globaltimer() - t0 > kTimeoutNs) {
             report_error(prm.status, BAK_ETIMEOUT);
             my_abort = 1;
@@ -201,153 +204,178 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepParams prm) {
           }
         }
       }
-      T sp = T(0), sq = T(0);
-      for (uint32_t r = 0; r < G; ++r) {
-        sp = Num<T>::add(sp, static_cast<T>(xslot[buf * kMaxCluster + r].p));
-        if (with_q) sq = Num<T>::add(sq, static_cast<T>(xslot[buf * kMaxCluster + r].q));
+      c = meta_col[ls];
+      n2 = static_cast<T>(meta_n2[ls]);
+      const T* X = xs + static_cast<size_t>(ls) * prm.stage_elems;
+#pragma unroll
+      for (int k = 0; k < E; ++k) xr[k] = (k < kv) ? X[tid + k * NT] : T(0);
+      rel[nrel++] = ls;
+      if (++ls == S) { ls = 0; lph ^= 1u; }
+    };
+
+    // reduction across all participants; returns true on (uniform) abort
+    auto reduce = [&](T pv, T qv, bool with_q, uint32_t rc, T& P, T& Q) -> bool {
+      const int buf = rc & 1;
+      pv = warp_sum(pv);
+      if (with_q) qv = warp_sum(qv);
+      if (lane == 0) {
+        red[(buf * 2 + 0) * 32 + warp] = pv;
+        red[(buf * 2 + 1) * 32 + warp] = qv;
       }
-      P = sp;
-      Q = sq;
-      return false;
-    }
-    // kModeGrid: epoch-tagged records in global memory
-    const uint32_t epoch = rc + 1;
-    uint32_t* slots = prm.slots + static_cast<size_t>(buf) * G * 8;
-    if (tid == 0) {
-      ll_store(slots + static_cast<size_t>(rank) * 8, static_cast<double>(bp), epoch);
-      if (with_q) ll_store(slots + static_cast<size_t>(rank) * 8 + 4, static_cast<double>(bq), epoch);
-      if (refill && issued < total) {
-        const int s = static_cast<int>(issued % S);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + pcol * prm.ldx + r0, bytes, &full[s], pol);
-        pc.next();
-        ++issued;
-        if (issued < total) pcol = pc.col();
+      if (bar_or(NT, my_abort)) return true;
+      // all consumers have pulled their stages into registers: hand them back
+      if (tid == 0) {
+        for (int i = 0; i < nrel; ++i) mbar_arrive(&empty[rel[i]]);
       }
-    }
-    if (warp == 0) {
-      T sp = T(0), sq = T(0);
-      const uint64_t t0 = globaltimer();
-      bool timed_out = false;
-      for (uint32_t i = lane; i < G; i += 32) {
-        double v;
-        while (!ll_load(slots + static_cast<size_t>(i) * 8, epoch, v)) {
-          if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+      nrel = 0;
+      T bp = T(0), bq = T(0);
+      for (int w = 0; w < nwarps; ++w) bp = Num<T>::add(bp, red[(buf * 2 + 0) * 32 + w]);
+      if (with_q)
+        for (int w = 0; w < nwarps; ++w) bq = Num<T>::add(bq, red[(buf * 2 + 1) * 32 + w]);
+      if (MODE == kModeCta) {
+        P = bp;
+        Q = bq;
+        return false;
+      }
+      if (MODE == kModeCluster) {
+        if (tid < static_cast<int>(G)) {
+          const uint32_t rs = mapa(smem_addr(&xslot[buf * kMaxCluster + rank]), tid);
+          const uint32_t rb = mapa(smem_addr(&xbar[buf]), tid);
+          st_async_v2(rs, static_cast<double>(bp), static_cast<double>(bq), rb);
         }
-        sp = Num<T>::add(sp, static_cast<T>(v));
-        if (with_q) {
-          while (!ll_load(slots + static_cast<size_t>(i) * 8 + 4, epoch, v)) {
+        if (tid == 0) mbar_arrive_expect_tx(&xbar[buf], G * 16u);
+        const uint32_t par = (rc >> 1) & 1;
+        if (!mbar_test_cluster(&xbar[buf], par)) {
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test_cluster(&xbar[buf], par)) {
+            if (globaltimer() - t0 > kTimeoutNs) {
+              report_error(prm.status, BAK_ETIMEOUT);
+              my_abort = 1;
+              break;
+            }
+          }
+        }
+        T sp = T(0), sq = T(0);
+        for (uint32_t r = 0; r < G; ++r) {
+          sp = Num<T>::add(sp, static_cast<T>(xslot[buf * kMaxCluster + r].p));
+          if (with_q) sq = Num<T>::add(sq, static_cast<T>(xslot[buf * kMaxCluster + r].q));
+        }
+        P = sp;
+        Q = sq;
+        return false;
+      }
+      // kModeGrid: epoch-tagged records in global memory
+      const uint32_t epoch = rc + 1;
+      uint32_t* slots = prm.slots + static_cast<size_t>(buf) * G * 8;
+      if (tid == 0) {
+        ll_store(slots + static_cast<size_t>(rank) * 8, static_cast<double>(bp), epoch);
+        if (with_q) ll_store(slots + static_cast<size_t>(rank) * 8 + 4, static_cast<double>(bq), epoch);
+      }
+      if (warp == 0) {
+        T sp = T(0), sq = T(0);
+        const uint64_t t0 = globaltimer();
+        bool timed_out = false;
+        for (uint32_t i = lane; i < G; i += 32) {
+          double v;
+          while (!ll_load(slots + static_cast<size_t>(i) * 8, epoch, v)) {
             if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
           }
-          sq = Num<T>::add(sq, static_cast<T>(v));
+          sp = Num<T>::add(sp, static_cast<T>(v));
+          if (with_q) {
+            while (!ll_load(slots + static_cast<size_t>(i) * 8 + 4, epoch, v)) {
+              if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+            }
+            sq = Num<T>::add(sq, static_cast<T>(v));
+          }
         }
+        if (timed_out) {
+          report_error(prm.status, BAK_ETIMEOUT);
+          my_abort = 1;
+        }
+        sp = warp_sum(sp);
+        if (with_q) sq = warp_sum(sq);
+        if (lane == 0) bcast[buf] = Pair{static_cast<double>(sp), static_cast<double>(sq)};
       }
-      if (timed_out) {
-        report_error(prm.status, BAK_ETIMEOUT);
-        my_abort = 1;
-      }
-      sp = warp_sum(sp);
-      if (with_q) sq = warp_sum(sq);
-      if (lane == 0) bcast[buf] = Pair<T>{static_cast<double>(sp), static_cast<double>(sq)};
-    }
-    const bool any2 = __syncthreads_or(my_abort) != 0;
-    P = static_cast<T>(bcast[buf].p);
-    Q = static_cast<T>(bcast[buf].q);
-    return any2;
-  };
+      const bool any2 = bar_or(NT, my_abort);
+      P = static_cast<T>(bcast[buf].p);
+      Q = static_cast<T>(bcast[buf].q);
+      return any2;
+    };
 
-  // ---- prologue: dot for the first column ----
-  uint32_t rc = 0;
-  T P, Q;
-  bool aborted = false;
-  {
-    wait_stage(0);
-    const T* X0 = xs;
+    // ---- prologue: columns 0 and 1 into registers, dot for column 0 ----
+    uint32_t rc = 0;
+    T P = T(0), Q = T(0);
+    int64_t c0 = 0, c1 = 0;
+    T n2_0 = T(1), n2_1 = T(1);
+    pull(xc, c0, n2_0);
+    if (total > 1) pull(xn, c1, n2_1);
     T pv = T(0);
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const T xv = (k < kv) ? X0[tid + k * NT] : T(0);
-      pv = Num<T>::fma(xv, ev[k], pv);
-    }
-    aborted = reduce(pv, T(0), false, rc++, false, P, Q);
-  }
+    for (int k = 0; k < E; ++k) pv = Num<T>::fma(xc[k], ev[k], pv);
+    bool aborted = reduce(pv, T(0), false, rc++, P, Q);
 
-  ColCursor cc{prm.cols, ncols, prm.cols_stride, 0, 0};
-  int64_t c_cur = cc.col();
-  T n2_cur = n2g[c_cur];
-  cc.next();
-  int64_t c_next = (total > 1) ? cc.col() : c_cur;
-  T n2_next = n2g[c_next];
-  const bool updater = (rank == 0) && (tid == (NT > 32 ? 32 : 0));
-  T a_val = updater ? ag[c_cur] : T(0);
+    const bool updater = (rank == 0) && (tid == (NT > 32 ? 32 : 0));
+    T a0 = updater ? ag[c0] : T(0);
+    T a1 = (updater && total > 1) ? ag[c1] : T(0);
 
-  int64_t sweep = 0, k = 0, t = 0;
-  bool converged = false;
-  while (!aborted) {
-    const T d = Num<T>::div(P, n2_cur);
-    const bool last = (k == ncols - 1);
-    const bool has_next = !(last && sweep + 1 == prm.max_iter);
-    const T* Xc = xs + static_cast<size_t>(t % S) * prm.stage_elems;
-    const T* Xn = xs + static_cast<size_t>((t + 1) % S) * prm.stage_elems;
-    if (has_next) wait_stage(t + 1);
-    T pv = T(0), qv = T(0);
+    int64_t sweep = 0, k = 0, t = 0;
+    bool converged = false;
+    while (!aborted) {
+      const T d = Num<T>::div(P, n2_0);
+      const bool last = (k == ncols - 1);
+      const bool has_next = !(last && sweep + 1 == prm.max_iter);
+      T qv = T(0);
+      pv = T(0);
 #pragma unroll
-    for (int kk = 0; kk < E; ++kk) {
-      const bool ok = kk < kv;
-      const T xc = ok ? Xc[tid + kk * NT] : T(0);
-      ev[kk] = Num<T>::sub(ev[kk], Num<T>::mul(xc, d));
-      if (has_next) {
-        const T xn = ok ? Xn[tid + kk * NT] : T(0);
-        pv = Num<T>::fma(xn, ev[kk], pv);
+      for (int kk = 0; kk < E; ++kk) {
+        ev[kk] = Num<T>::sub(ev[kk], Num<T>::mul(xc[kk], d));
+        if (has_next) pv = Num<T>::fma(xn[kk], ev[kk], pv);
+        if (last) qv = Num<T>::fma(ev[kk], ev[kk], qv);
       }
-      if (last) qv = Num<T>::fma(ev[kk], ev[kk], qv);
-    }
-    if (updater) {
-      a_val = Num<T>::add(a_val, d);
-      ag[c_cur] = a_val;
-      if (has_next) a_val = ag[c_next];  // same-thread store->load: sees the new value if c_next == c_cur
-    }
-    aborted = reduce(pv, qv, last, rc++, true, P, Q);
-    if (aborted) break;
-    if (last) {
-      if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
-      ++sweep;
-      if (prm.thresh2 >= 0.0 && static_cast<double>(Q) <= prm.thresh2) {
-        converged = true;
-        break;
-      }
-      if (sweep == prm.max_iter) break;
-      k = 0;
-    } else {
-      ++k;
-    }
-    ++t;
-    c_cur = c_next;
-    n2_cur = n2_next;
-    cc.next();
-    if (t + 1 < total) {
-      c_next = cc.col();
-      n2_next = n2g[c_next];
-    }
-  }
-
-  // ---- epilogue ----
+      int64_t c2 = c1;
+      T n2_2 = n2_1;
 #pragma unroll
-  for (int kk = 0; kk < E; ++kk)
-    if (kk < kv) eg[r0 + tid + static_cast<int64_t>(kk) * NT] = ev[kk];
-  if (tid == 0) {
-    // drain bulk copies still in flight into this CTA's ring
-    for (int64_t u = t + 2; u < issued; ++u) {
-      const int s = static_cast<int>(u % S);
-      const uint32_t par = static_cast<uint32_t>((u / S) & 1);
-      const uint64_t t0 = globaltimer();
-      while (!mbar_test(&full[s], par))
-        if (globaltimer() - t0 > kTimeoutNs) break;
+      for (int kk = 0; kk < E; ++kk) xc[kk] = xn[kk];
+      if (t + 2 < total) pull(xn, c2, n2_2);
+      if (updater) {
+        const T na = Num<T>::add(a0, d);
+        ag[c0] = na;
+        if (c1 == c0) a1 = na;
+        a0 = a1;
+        if (t + 2 < total) a1 = ag[c2];  // store->load order in one thread: never stale
+      }
+      aborted = reduce(pv, qv, last, rc++, P, Q);
+      if (aborted) break;
+      if (last) {
+        if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
+        ++sweep;
+        if (prm.thresh2 >= 0.0 && static_cast<double>(Q) <= prm.thresh2) {
+          converged = true;
+          break;
+        }
+        if (sweep == prm.max_iter) break;
+        k = 0;
+      } else {
+        ++k;
+      }
+      ++t;
+      c0 = c1;
+      n2_0 = n2_1;
+      c1 = c2;
+      n2_1 = n2_2;
     }
-    if (rank == 0 && prm.status) {
-      prm.status[0] = sweep;
-      prm.status[1] = converged ? 1 : 0;
-      prm.status[3] = MODE == kModeCta ? BAK_VARIANT_CTA : (MODE == kModeCluster ? BAK_VARIANT_CLUSTER : BAK_VARIANT_GRID);
+
+#pragma unroll
+    for (int kk = 0; kk < E; ++kk)
+      if (kk < kv) eg[r0 + tid + static_cast<int64_t>(kk) * NT] = ev[kk];
+    if (tid == 0) {
+      *stop = 1;
+      if (rank == 0 && prm.status) {
+        prm.status[0] = sweep;
+        prm.status[1] = converged ? 1 : 0;
+        prm.status[3] =
+            MODE == kModeCta ? BAK_VARIANT_CTA : (MODE == kModeCluster ? BAK_VARIANT_CLUSTER : BAK_VARIANT_GRID);
+      }
     }
   }
   __syncthreads();
@@ -357,7 +385,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepParams prm) {
 // ------------------------------- host -------------------------------------
 
 size_t smem_bytes(const SweepPlan& pl, size_t tsize) {
-  return static_cast<size_t>(pl.nstages) * pl.stage_elems * tsize + kMaxStages * 8 + 2 * 2 * 32 * tsize + 16 +
+  return static_cast<size_t>(pl.nstages) * pl.stage_elems * tsize + 4 * kMaxStages * 8 + 2 * 2 * 32 * tsize + 16 +
          2 * kMaxCluster * 16 + 16 + 32 + 16;
 }
 
@@ -368,7 +396,7 @@ int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.nparticipants);
-  cfg.blockDim = dim3(pl.nthreads);
+  cfg.blockDim = dim3(pl.nthreads + 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -412,63 +440,78 @@ int launch_e(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
 // ---- planning: pick participants, threads, rows per thread, stages ----
 static const int kEs[] = {1, 2, 4, 8, 16, 32};
 
-bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
+static bool plan_fill(int dtype, int variant, int64_t obs, int nthreads, int e, int parts, SweepPlan& pl,
+                      int min_stages) {
   const size_t ts = dtype_size(dtype);
+  const size_t smem_cap = static_cast<size_t>(device_max_smem_optin()) - 2048;
+  const int64_t rows = static_cast<int64_t>(nthreads) * e;
+  if (nthreads < 32 || nthreads > kMaxConsumers || nthreads % 32) return false;
+  if (rows * parts < obs || (parts - 1) * rows >= obs) return false;
+  SweepPlan cand;
+  cand.variant = variant;
+  cand.nthreads = nthreads;
+  cand.e = e;
+  cand.nparticipants = parts;
+  cand.rows_per_cta = rows;
+  cand.stage_elems = rows;
+  cand.nstages = 0;
+  const size_t fixed = smem_bytes(cand, ts);
+  const size_t stage_bytes = rows * ts;
+  if (fixed + 2 * stage_bytes > smem_cap) return false;
+  int s = static_cast<int>((smem_cap - fixed) / stage_bytes);
+  if (s > kMaxStages) s = kMaxStages;
+  if (s < min_stages) return false;
+  cand.nstages = s;
+  pl = cand;
+  return true;
+}
+
+// BAK_PLAN="parts,e,nthreads" overrides the heuristic (tuning experiments)
+static bool plan_env(int dtype, int variant, int64_t obs, SweepPlan& pl) {
+  const char* env = getenv("BAK_PLAN");
+  if (!env) return false;
+  int parts = 0, e = 0, nt = 0;
+  if (sscanf(env, "%d,%d,%d", &parts, &e, &nt) != 3) return false;
+  return plan_fill(dtype, variant, obs, nt, e, parts, pl, 2);
+}
+
+bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
   const int sms = device_sms();
-  const size_t smem_cap = static_cast<size_t>(device_max_smem_optin()) - 4096;
-  pl.variant = variant;
-  auto fits = [&](int nthreads, int e, int parts) -> bool {
-    const int64_t rows = static_cast<int64_t>(nthreads) * e;
-    if (rows * parts < obs) return false;
-    pl.nthreads = nthreads;
-    pl.e = e;
-    pl.nparticipants = parts;
-    pl.rows_per_cta = rows;
-    pl.stage_elems = rows;
-    const size_t stage_bytes = rows * ts;
-    int s = static_cast<int>((smem_cap - 2048) / stage_bytes);
-    if (s > kMaxStages) s = kMaxStages;
-    if (s < 2) return false;
-    pl.nstages = s;
-    return true;
-  };
+  if (plan_env(dtype, variant, obs, pl)) return true;
+  const int max_e = dtype == BAK_F64 ? 8 : 16;
   if (variant == BAK_VARIANT_CTA) {
-    // short columns: favour few warps (short reduction tree), E <= 32
+    // short columns: smallest E that fits 256 consumer threads, else larger E / more threads
     for (int e : kEs) {
-      int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
-      if (nt <= 256 && fits(nt < 32 ? 32 : nt, e, 1)) return true;
+      if (e > max_e) break;
+      const int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
+      if (nt <= 256 && plan_fill(dtype, variant, obs, nt, e, 1, pl, 4)) return true;
     }
     for (int e : kEs) {
-      int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
-      if (nt <= 512 && fits(nt, e, 1)) return true;
+      const int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
+      if (plan_fill(dtype, variant, obs, nt, e, 1, pl, 2)) return true;
     }
     return false;
   }
   if (variant == BAK_VARIANT_CLUSTER) {
-    for (int c = 2; c <= kMaxCluster; c *= 2) {
+    for (int c : {2, 4, 8, 16}) {
       const int64_t per = (obs + c - 1) / c;
       for (int e : kEs) {
-        int nt = static_cast<int>(round_up((per + e - 1) / e, 32));
-        if (nt <= 256 && fits(nt, e, c)) {
-          // shrink participants if rows_per_cta leaves a CTA empty
-          pl.nparticipants = static_cast<int>((obs + pl.rows_per_cta - 1) / pl.rows_per_cta);
-          if (pl.nparticipants < 2) pl.nparticipants = 2;
-          if (pl.nparticipants == 3) pl.nparticipants = 4;
-          if (pl.nparticipants > 4 && pl.nparticipants < 8) pl.nparticipants = 8;
-          if (pl.nparticipants > 8) pl.nparticipants = 16;
-          if ((pl.nparticipants - 1) * pl.rows_per_cta >= obs) continue;
-          return true;
-        }
+        if (e > max_e) break;
+        const int nt = static_cast<int>(round_up((per + e - 1) / e, 32));
+        if (nt > 256) continue;
+        int parts = static_cast<int>((obs + static_cast<int64_t>(nt) * e - 1) / (static_cast<int64_t>(nt) * e));
+        if (parts < 2) parts = 2;
+        if (plan_fill(dtype, variant, obs, nt, e, parts, pl, 4)) return true;
       }
     }
     return false;
   }
   if (variant == BAK_VARIANT_GRID) {
-    for (int nt : {256, 512}) {
+    for (int nt : {256}) {
       for (int e : kEs) {
         const int64_t rows = static_cast<int64_t>(nt) * e;
         const int64_t parts = (obs + rows - 1) / rows;
-        if (parts <= sms && fits(nt, e, static_cast<int>(parts)) && pl.nstages >= 3) return true;
+        if (parts <= sms && plan_fill(dtype, variant, obs, nt, e, static_cast<int>(parts), pl, 3)) return true;
       }
     }
     return false;

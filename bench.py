@@ -292,7 +292,7 @@ def run_ours(args, cfg, rank, world, dev):
         k_sweeps = int(r.sweeps_run.max())
         kernel = "batched_kernel (whole per-system solve, one CTA per system)"
     else:
-        ws = _Workspace(torch, dev, _workspace_bytes(lib, code, dm.obs, dm.vars))
+        ws = _Workspace(torch, dev, _workspace_bytes(lib, code, dm.obs, dm.vars, _lib.VARIANTS[args.variant]))
         norms = pb.colnorms(dm, ws)
         e = torch.empty_like(y)
         a = torch.zeros(dm.vars, dtype=y.dtype, device=dev)

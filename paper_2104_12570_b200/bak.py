@@ -11,7 +11,9 @@ kernels.  There is no CPU fallback: without a CUDA device or without the
 library this module raises.
 
 Extensions (keyword-only, defaults keep reference behaviour):
-    variant="auto"|"cta"|"cluster"|"grid"|"stream"   kernel family
+    variant="auto"|"cta"|"cluster"|"grid"|"stream"   exact per-column kernel family
+            |"gram"                                   labelled algebraically-equivalent sweep
+                                                      (one x pass per sweep via G = X^T X)
     device=None                                       torch device (default current CUDA device)
     return_device=False                               keep a_hat/residual as CUDA tensors
 """
@@ -192,9 +194,9 @@ class _Workspace:
         return self.buf.numel()
 
 
-def _workspace_bytes(lib, code, obs, nv):
+def _workspace_bytes(lib, code, obs, nv, vcode=0):
     return max(lib.bak_colnorms_workspace(code, obs, nv), lib.bak_colnorms_workspace(code, obs, 1),
-               lib.bak_residual_workspace(code, obs, nv), lib.bak_sweep_workspace(code, 0, obs, nv), 4096)
+               lib.bak_residual_workspace(code, obs, nv), lib.bak_sweep_workspace(code, vcode, obs, nv), 4096)
 
 
 def colnorms(dm: DeviceMatrix, ws=None):
@@ -256,7 +258,7 @@ def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto
     st = _stream_ptr(torch, dev)
 
     t0 = time.perf_counter()
-    ws = _Workspace(torch, dev, _workspace_bytes(lib, code, obs, nv))
+    ws = _Workspace(torch, dev, _workspace_bytes(lib, code, obs, nv, _lib.VARIANTS[variant]))
     ynorm2 = float(_sumsq(lib, torch, code, yd, ws, st).item())
     if ynorm2 == 0.0:  # bak.py:168-170 (_zero_report)
         a_z = torch.zeros(nv, dtype=yd.dtype, device=dev)

@@ -46,6 +46,8 @@ def build(verbose=False, force=False):
                "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
+        if os.environ.get("BAK_PHASES"):
+            cmd.insert(1, "-DBAK_PHASES")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     failed = False
     for src, p in procs:

@@ -54,7 +54,7 @@ int device_max_smem_optin() {
 using namespace bak;
 
 namespace {
-constexpr int64_t kSlotBytes = 2 * 1024 * 32;  // 2 buffers x up to 1024 CTAs x 32 B records
+constexpr int64_t kSlotBytes = kGridSlotBytes;  // grid / stream exchange records
 
 int pick_variant(int dtype, int64_t obs) {
   SweepPlan pl;
@@ -81,10 +81,10 @@ extern "C" int bak_sweep_pick_variant(int dtype, int64_t obs, int64_t vars) {
 }
 
 extern "C" int64_t bak_sweep_workspace(int dtype, int variant, int64_t obs, int64_t vars) {
-  (void)dtype;
-  (void)variant;
-  (void)obs;
-  (void)vars;
+  if (variant == BAK_VARIANT_GRAM) {
+    const int64_t g = gram_workspace_bytes(dtype, obs, vars);
+    return g > kSlotBytes ? g : kSlotBytes;
+  }
   return kSlotBytes;
 }
 
@@ -133,6 +133,7 @@ extern "C" int bak_sweep(int dtype, int variant, const void* x, int64_t obs, int
   prm.history = history;
   prm.status = status;
   prm.slots = static_cast<uint32_t*>(workspace);
+  if (variant == BAK_VARIANT_GRAM) return launch_gram(dtype, prm, vars, workspace, workspace_bytes, st);
   if (variant == BAK_VARIANT_STREAM) {
     StreamPlan sp;
     if (!plan_stream(dtype, obs, sp)) {

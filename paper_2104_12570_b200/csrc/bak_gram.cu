@@ -1,0 +1,334 @@
+// GRAM variant (BAK_VARIANT_GRAM): an ALGEBRAICALLY EQUIVALENT reformulation of
+// the column sweep for tall systems whose residual e cannot stay on chip.
+// Labelled as such everywhere it is reported: same iterates in exact
+// arithmetic, different rounding than the reference's per-column dots.
+//
+// One SolveBak sweep (bak.py:92-112) over columns j1, j2, ... in order is
+//     d_j = <x_j, e_current> / n2_j,   e_current = e_start - sum_{k before j} d_k x_k
+//         = (g_j - sum_{k before j} G_jk d_k) / n2_j,   g = X^T e_start,  G = X^T X
+// followed by e_end = e_start - X d.  So a sweep needs ONE pass over x:
+//     pass(s):  e <- e - X d^(s)  (rows in parallel),  sum e^2,  g <- X^T e
+//     solve(s+1): forward substitution over the sweep order with G (vars x vars)
+// The per-column exact kernels must read x twice per column when e lives in
+// HBM (x_j for the update, x_{j+1} for the next dot, plus e in and out); this
+// variant reads x once per sweep plus e once, at the price of a one-time
+// G = X^T X (hand-written fp64 DMMA SYRK, fp64 accumulation for both precisions).
+//
+// pass kernel layout: thread (c, r) owns row r of a 256/nch-row tile and the
+// 16-column chunk c; its 16 x values live in registers (coalesced loads along
+// rows), are used for both the update and the dot, and the next tile's values
+// are prefetched while the current one is reduced.
+#include <cstdio>
+
+#include "bak_common.cuh"
+#include "bak_sweep.cuh"
+
+namespace bak {
+namespace {
+
+constexpr int kGT = 256;  // threads per pass CTA
+constexpr int kCW = 16;   // columns per thread chunk
+
+struct GramCtrl {
+  int64_t done, sweeps, converged, pad;
+};
+
+struct PassParams {
+  const void* x;
+  int64_t obs, ldx, vars;
+  void* e;
+  const double* delta;
+  int apply, dot;
+  double* gpart;
+  double* sqpart;
+  const GramCtrl* ctrl;
+};
+
+__host__ __device__ inline int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kGT, 2) gram_pass_kernel(const PassParams p) {
+  if (*reinterpret_cast<const volatile int64_t*>(&p.ctrl->done)) return;
+  __shared__ double dsh[512];
+  __shared__ double red[2][kGT];
+  __shared__ double es[2][kGT];
+  const int V = static_cast<int>(p.vars);
+  const int nch = pow2_at_least((V + kCW - 1) / kCW);
+  const int R = kGT / nch;  // rows per tile
+  const int tid = threadIdx.x;
+  const int c = tid / R, r = tid % R;
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ e = static_cast<T*>(p.e);
+  for (int j = tid; j < V; j += kGT) dsh[j] = p.apply ? p.delta[j] : 0.0;
+  __syncthreads();
+
+  const int64_t ntiles = (p.obs + R - 1) / R;
+  double acc[kCW];
+#pragma unroll
+  for (int q = 0; q < kCW; ++q) acc[q] = 0.0;
+  double sq = 0.0;
+  int jv[kCW];
+#pragma unroll
+  for (int q = 0; q < kCW; ++q) jv[q] = c * kCW + q;
+
+  T xa[kCW], xb[kCW];
+  T ea = T(0), eb = T(0);
+  auto load = [&](int64_t tile, T (&xr)[kCW], T& ev) {
+    const int64_t row = tile * R + r;
+    const bool ok = tile < ntiles && row < p.obs;
+#pragma unroll
+    for (int q = 0; q < kCW; ++q) xr[q] = (ok && jv[q] < V) ? __ldcs(x + jv[q] * p.ldx + row) : T(0);
+    if (c == 0) ev = ok ? e[row] : T(0);
+  };
+  int64_t tile = blockIdx.x;
+  load(tile, xa, ea);
+  int buf = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    load(tile + gridDim.x, xb, eb);  // prefetch the next tile (x and e)
+    const int64_t row = tile * R + r;
+    const bool ok = row < p.obs;
+    if (p.apply) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kCW; ++q) t = __fma_rn(static_cast<double>(xa[q]), dsh[jv[q] < V ? jv[q] : 0], t);
+      red[buf][tid] = t;
+    }
+    __syncthreads();
+    if (c == 0) {
+      double ev = static_cast<double>(ea);
+      if (p.apply) {
+        double tt = 0.0;
+        for (int cc = 0; cc < nch; ++cc) tt += red[buf][cc * R + r];
+        const T en = static_cast<T>(ev - tt);
+        if (ok) e[row] = en;
+        ev = static_cast<double>(en);
+        sq = __fma_rn(ev, ev, sq);
+      }
+      es[buf][r] = ev;
+    }
+    __syncthreads();
+    if (p.dot) {
+      const double er = es[buf][r];
+#pragma unroll
+      for (int q = 0; q < kCW; ++q) acc[q] = __fma_rn(static_cast<double>(xa[q]), er, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kCW; ++q) xa[q] = xb[q];
+    ea = eb;
+    buf ^= 1;
+  }
+  __syncthreads();
+  // per-column partials: reduce over the R row-threads of each chunk (fixed order)
+  double* gsh = &red[0][0];  // reuse 2*kGT doubles: process kCW/2 columns per round
+  for (int q0 = 0; q0 < kCW; q0 += 2) {
+    gsh[tid * 2 + 0] = acc[q0];
+    gsh[tid * 2 + 1] = acc[q0 + 1];
+    __syncthreads();
+    if (tid < nch * 2) {
+      const int cc = tid >> 1, qq = tid & 1;
+      const int j = cc * kCW + q0 + qq;
+      double s = 0.0;
+      for (int rr = 0; rr < R; ++rr) s += gsh[(cc * R + rr) * 2 + qq];
+      if (j < V && p.dot) p.gpart[static_cast<int64_t>(blockIdx.x) * V + j] = s;
+    }
+    __syncthreads();
+  }
+  // sum e^2 of this CTA
+  double s2 = warp_sum(sq);
+  if ((tid & 31) == 0) gsh[tid >> 5] = s2;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kGT / 32; ++w) s += gsh[w];
+    p.sqpart[blockIdx.x] = s;
+  }
+}
+
+struct SolveParams {
+  int64_t vars, nblk;
+  int64_t sweep;  // sweep about to be solved (1-based); finalizes sweep-1
+  int64_t max_iter;
+  double thresh2;
+  const int32_t* cols;
+  int64_t ncols, cols_stride;
+  const void* norms2;
+  const double* G;
+  const double* gpart;
+  const double* sqpart;
+  void* a;
+  double* delta;
+  double* history;
+  GramCtrl* ctrl;
+  int64_t* status;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p) {
+  if (p.ctrl->done) return;
+  __shared__ double dsh[2];
+  __shared__ double wsum[16];
+  const int V = static_cast<int>(p.vars);
+  const int tid = threadIdx.x;
+  const int s = static_cast<int>(p.sweep);
+  if (s >= 2) {
+    // finalize sweep s-1: sum e^2 over the pass CTAs in fixed order
+    double v = 0.0;
+    for (int64_t b = tid; b < p.nblk; b += blockDim.x) v += p.sqpart[b];
+    v = warp_sum(v);
+    if ((tid & 31) == 0) wsum[tid >> 5] = v;
+    __syncthreads();
+    double sq = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x) / 32; ++w) sq += wsum[w];
+    const bool stop_conv = p.thresh2 >= 0.0 && sq <= p.thresh2;
+    const bool stop_max = (s - 1) >= p.max_iter;
+    if (tid == 0) {
+      if (p.history) p.history[s - 2] = sq;
+      if (stop_conv || stop_max) {
+        p.ctrl->done = 1;
+        p.ctrl->sweeps = s - 1;
+        p.ctrl->converged = stop_conv ? 1 : 0;
+        if (p.status) {
+          p.status[0] = s - 1;
+          p.status[1] = stop_conv ? 1 : 0;
+          p.status[3] = BAK_VARIANT_GRAM;
+        }
+      }
+    }
+    if (stop_conv || stop_max) return;
+  }
+  // g = sum over pass CTAs (fixed order), residual dots in double
+  __shared__ int ord[512];
+  __shared__ double n2s[512];
+  const T* n2 = static_cast<const T*>(p.norms2);
+  T* a = static_cast<T*>(p.a);
+  const int32_t* cl = p.cols ? p.cols + (p.cols_stride ? (s - 1) * p.cols_stride : 0) : nullptr;
+  for (int64_t kk = tid; kk < p.ncols; kk += blockDim.x) ord[kk] = cl ? cl[kk] : static_cast<int>(kk);
+  double rj = 0.0;
+  T aj = T(0);
+  if (tid < V) {
+    for (int64_t b = 0; b < p.nblk; ++b) rj += p.gpart[b * V + tid];
+    n2s[tid] = static_cast<double>(n2[tid]);
+    aj = a[tid];
+  }
+  double dj = 0.0;
+  __syncthreads();
+  // forward substitution over the sweep order; G column of the next step prefetched
+  double gnext = (tid < V && p.ncols > 0) ? p.G[static_cast<int64_t>(ord[0]) * V + tid] : 0.0;
+  for (int64_t kk = 0; kk < p.ncols; ++kk) {
+    const int j = ord[kk];
+    const double gcol = gnext;
+    if (tid < V && kk + 1 < p.ncols) gnext = p.G[static_cast<int64_t>(ord[kk + 1]) * V + tid];
+    if (tid == j) {
+      const T d = Num<T>::div(static_cast<T>(rj), static_cast<T>(n2s[j]));
+      dsh[kk & 1] = static_cast<double>(d);
+      dj = static_cast<double>(d);
+      aj = Num<T>::add(aj, d);
+    }
+    __syncthreads();
+    if (tid < V) rj = __fma_rn(-gcol, dsh[kk & 1], rj);
+  }
+  if (tid < V) {
+    p.delta[tid] = dj;  // 0 for columns not in this sweep's list (zero norms)
+    a[tid] = aj;
+  }
+}
+
+}  // namespace
+
+// workspace layout (bytes): G | gpart | sqpart | delta | ctrl | G partials (split-K)
+static int64_t gram_nblk() { return 2 * static_cast<int64_t>(device_sms()); }
+
+int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars) {
+  (void)dtype;
+  int64_t b = 0;
+  b += vars * vars * 8;
+  b += gram_nblk() * vars * 8;
+  b += gram_nblk() * 8;
+  b += vars * 8;
+  b += 64;
+  int nchunks;
+  int64_t chunk;
+  b += gram_g_workspace(obs, vars, nchunks, chunk) + 256;
+  return round_up(b, 256) + 4096;
+}
+
+bool gram_supported(int64_t vars) { return vars >= 1 && vars <= 512; }
+
+int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st) {
+  if (!gram_supported(vars)) {
+    set_error("GRAM variant supports 1 <= vars <= 512 (got %lld)", (long long)vars);
+    return BAK_EUNSUPPORTED;
+  }
+  if (wsb < gram_workspace_bytes(dtype, prm.obs, vars)) {
+    set_error("bak_sweep(GRAM): workspace too small (need %lld)", (long long)gram_workspace_bytes(dtype, prm.obs, vars));
+    return BAK_EWORKSPACE;
+  }
+  const int64_t nblk = gram_nblk();
+  char* w = static_cast<char*>(ws);
+  double* G = reinterpret_cast<double*>(w);
+  w += vars * vars * 8;
+  double* gpart = reinterpret_cast<double*>(w);
+  w += nblk * vars * 8;
+  double* sqpart = reinterpret_cast<double*>(w);
+  w += nblk * 8;
+  double* delta = reinterpret_cast<double*>(w);
+  w += vars * 8;
+  GramCtrl* ctrl = reinterpret_cast<GramCtrl*>(w);
+  w += 64;
+  double* gparts_ws = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
+  const int64_t gparts_bytes = wsb - (reinterpret_cast<char*>(gparts_ws) - static_cast<char*>(ws));
+
+  // ---- G = X^T X: hand-written fp64 DMMA SYRK (bak_gram_dmma.cu) ----
+  if (int rc = launch_gram_g(dtype, prm.x, prm.obs, prm.ldx, vars, G, gparts_ws, gparts_bytes, st)) return rc;
+  BAK_CHECK_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(GramCtrl), st));
+
+  PassParams pp{prm.x, prm.obs, prm.ldx, vars, prm.e, delta, 0, 1, gpart, sqpart, ctrl};
+  SolveParams sp{vars, nblk, 0, prm.max_iter, prm.thresh2, prm.cols, prm.ncols, prm.cols_stride, prm.norms2,
+                 G, gpart, sqpart, prm.a, delta, prm.history, ctrl, prm.status};
+  const bool use_tma = gram_tma_supported(vars);
+  if (use_tma) sp.nblk = gram_tma_grid();
+  auto pass = [&](int apply, int dot) -> int {
+    if (use_tma)
+      return launch_gram_pass_tma(dtype, prm.x, prm.obs, prm.ldx, vars, prm.e, delta, apply, dot, gpart, sqpart,
+                                  &ctrl->done, st);
+    pp.apply = apply;
+    pp.dot = dot;
+    if (dtype == BAK_F64)
+      gram_pass_kernel<double><<<static_cast<unsigned>(nblk), kGT, 0, st>>>(pp);
+    else
+      gram_pass_kernel<float><<<static_cast<unsigned>(nblk), kGT, 0, st>>>(pp);
+    count_launches(1);
+    BAK_CHECK_CUDA(cudaGetLastError());
+    return BAK_OK;
+  };
+  auto solve = [&](int64_t s) -> int {
+    sp.sweep = s;
+    if (dtype == BAK_F64)
+      gram_solve_kernel<double><<<1, 512, 0, st>>>(sp);
+    else
+      gram_solve_kernel<float><<<1, 512, 0, st>>>(sp);
+    count_launches(1);
+    BAK_CHECK_CUDA(cudaGetLastError());
+    return BAK_OK;
+  };
+  int rc = pass(0, 1);
+  if (rc) return rc;
+  for (int64_t s = 1; s <= prm.max_iter; ++s) {
+    if ((rc = solve(s))) return rc;
+    if ((rc = pass(1, s < prm.max_iter ? 1 : 0))) return rc;
+    if (prm.thresh2 >= 0.0 && s % 16 == 0) {
+      // early break: stop enqueueing once the device has flagged convergence
+      int64_t done = 0;
+      BAK_CHECK_CUDA(cudaMemcpyAsync(&done, &ctrl->done, sizeof(done), cudaMemcpyDeviceToHost, st));
+      BAK_CHECK_CUDA(cudaStreamSynchronize(st));
+      if (done) break;
+    }
+  }
+  return solve(prm.max_iter + 1);
+}
+
+}  // namespace bak

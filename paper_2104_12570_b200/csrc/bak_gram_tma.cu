@@ -1,0 +1,236 @@
+// GRAM pass kernel, TMA-fed (vars <= 256): one streaming pass over x per sweep
+//     e <- e - X d ,  sum e^2 ,  g <- X^T e          (see bak_gram.cu)
+//
+// Persistent grid, one CTA per SM = 8 consumer warps + 1 producer warp.  The
+// producer streams 32-row x vars tiles of column-major x with 2-D tensor-map
+// TMA (cp.async.bulk.tensor, out-of-range rows/columns zero-filled) into a
+// 3-stage shared-memory ring (full/empty mbarriers).  Consumer warp c owns the
+// column chunk [c*CW, (c+1)*CW), lane r owns tile row r: reads of a column
+// segment are conflict-free.  Per tile: chunk partials of (X d)_r -> named
+// barrier -> warp 0 finishes e_r (prefetched one tile ahead) -> named barrier
+// -> every warp accumulates x_rj * e_r for its columns.  x is read from HBM
+// exactly once per sweep; e once in, once out.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "bak_common.cuh"
+#include "bak_sweep.cuh"
+
+namespace bak {
+namespace {
+
+constexpr int kR = 32;       // rows per tile
+constexpr int kWarps = 8;    // consumer warps (= column chunks)
+constexpr int kS = 3;        // ring stages
+constexpr int kCons = kWarps * 32;
+
+struct TmaPassParams {
+  int64_t obs, vars, ntiles;
+  void* e;
+  const double* delta;
+  int apply, dot;
+  double* gpart;
+  double* sqpart;
+  const int64_t* done;
+};
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bar_cons() { asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory"); }
+
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+template <typename T, int CW>
+__global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __grid_constant__ CUtensorMap xmap,
+                                                                      const TmaPassParams p) {
+  if (*reinterpret_cast<const volatile int64_t*>(p.done)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int VB = CW * kWarps;  // tile columns (box width)
+  constexpr uint32_t kTileBytes = kR * VB * sizeof(T);
+  T* xs = reinterpret_cast<T*>(smem_raw);  // [kS][VB][kR] (column-major tile)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kS * kTileBytes);
+  uint64_t* empty = full + kS;
+  double* dsh = reinterpret_cast<double*>(empty + kS);  // [VB]
+  double* red = dsh + VB;                                // [kWarps][kR]
+  double* es = red + kWarps * kR;                        // [kR]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = static_cast<int>(p.vars);
+  if (tid == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  for (int j = tid; j < VB; j += blockDim.x) dsh[j] = (p.apply && j < V) ? p.delta[j] : 0.0;
+  __syncthreads();
+
+  if (warp == kWarps) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int64_t u = 0;
+      for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++u) {
+        if (u >= kS) {
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test(&empty[s], ph ^ 1u))
+            if (globaltimer() - t0 > kTimeoutNs) return;
+        }
+        mbar_arrive_expect_tx(&full[s], kTileBytes);
+        tma_2d(xs + static_cast<size_t>(s) * kR * VB, &xmap, static_cast<int>(tile * kR), 0, &full[s]);
+        if (++s == kS) { s = 0; ph ^= 1u; }
+      }
+    }
+    return;  // (consumers use named barrier 1 only; the final __syncthreads is not reached by this warp)
+  }
+  // ------------------------------ consumers ------------------------------
+  T* e = static_cast<T*>(p.e);
+  double acc[CW];
+#pragma unroll
+  for (int q = 0; q < CW; ++q) acc[q] = 0.0;
+  double sq = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  int prev = -1;
+  int64_t tile = blockIdx.x;
+  T e_next = T(0);
+  if (warp == 0 && tile < p.ntiles) {
+    const int64_t row = tile * kR + lane;
+    e_next = row < p.obs ? e[row] : T(0);
+  }
+  for (; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t row = tile * kR + lane;
+    const T e_cur = e_next;
+    if (warp == 0) {
+      const int64_t nrow = (tile + gridDim.x) * kR + lane;
+      e_next = (tile + gridDim.x < p.ntiles && nrow < p.obs) ? e[nrow] : T(0);
+    }
+    {
+      const uint64_t t0 = globaltimer();
+      while (!mbar_test(&full[s], ph))
+        if (globaltimer() - t0 > kTimeoutNs) break;
+    }
+    const T* X = xs + static_cast<size_t>(s) * kR * VB + static_cast<size_t>(warp) * CW * kR + lane;
+    if (p.apply) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < CW; ++q) t = __fma_rn(static_cast<double>(X[q * kR]), dsh[warp * CW + q], t);
+      red[warp * kR + lane] = t;
+    }
+    bar_cons();
+    if (tid == 0 && prev >= 0) mbar_arrive1(&empty[prev]);  // previous tile fully consumed
+    if (warp == 0) {
+      double ev = static_cast<double>(e_cur);
+      if (p.apply) {
+        double tt = 0.0;
+#pragma unroll
+        for (int c = 0; c < kWarps; ++c) tt += red[c * kR + lane];
+        const T en = static_cast<T>(ev - tt);
+        if (row < p.obs) e[row] = en;
+        ev = static_cast<double>(en);
+        sq = __fma_rn(ev, ev, sq);
+      }
+      es[lane] = ev;
+    }
+    bar_cons();
+    if (p.dot) {
+      const double er = es[lane];
+#pragma unroll
+      for (int q = 0; q < CW; ++q) acc[q] = __fma_rn(static_cast<double>(X[q * kR]), er, acc[q]);
+    }
+    prev = s;
+    if (++s == kS) { s = 0; ph ^= 1u; }
+  }
+  // column partials: sum over the 32 tile rows (lanes), fixed butterfly order
+  if (p.dot) {
+#pragma unroll
+    for (int q = 0; q < CW; ++q) {
+      const double v = warp_sum(acc[q]);
+      const int j = warp * CW + q;
+      if (lane == q && j < V) p.gpart[static_cast<int64_t>(blockIdx.x) * V + j] = v;
+    }
+  }
+  if (warp == 0) {
+    const double v = warp_sum(sq);
+    if (lane == 0) p.sqpart[blockIdx.x] = v;
+  }
+  bar_cons();
+  if (tid == 0 && prev >= 0) mbar_arrive1(&empty[prev]);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+template <typename T, int CW>
+int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStream_t st) {
+  constexpr int VB = CW * kWarps;
+  const size_t smem = kS * static_cast<size_t>(kR) * VB * sizeof(T) + 2 * kS * 8 + VB * 8 + kWarps * kR * 8 + kR * 8;
+  auto kern = gram_pass_tma_kernel<T, CW>;
+  BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<grid, kCons + 32, smem, st>>>(map, p);
+  count_launches(1);
+  BAK_CHECK_CUDA(cudaGetLastError());
+  return BAK_OK;
+}
+
+}  // namespace
+
+bool gram_tma_supported(int64_t vars) { return vars >= 1 && vars <= 256 && encode_fn() != nullptr; }
+
+int gram_tma_grid() { return device_sms(); }
+
+// x: column-major obs x vars, ldx*sizeof(T) % 16 == 0
+int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
+                         const double* delta, int apply, int dot, double* gpart, double* sqpart, const int64_t* done,
+                         cudaStream_t st) {
+  auto enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BAK_ECUDA;
+  }
+  const int cw = vars <= 64 ? 8 : (vars <= 128 ? 16 : 32);
+  const int vb = cw * kWarps;
+  const size_t ts = dtype == BAK_F64 ? 8 : 4;
+  CUtensorMap map;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(obs), static_cast<cuuint64_t>(vars)};
+  cuuint64_t gstr[1] = {static_cast<cuuint64_t>(ldx * ts)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kR), static_cast<cuuint32_t>(vb)};
+  cuuint32_t est[2] = {1, 1};
+  CUresult r = enc(&map, dtype == BAK_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(x), gdim, gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return BAK_ECUDA;
+  }
+  TmaPassParams p{obs, vars, (obs + kR - 1) / kR, e, delta, apply, dot, gpart, sqpart, done};
+  const int grid = gram_tma_grid();
+  if (dtype == BAK_F64) {
+    if (cw == 8) return launch_cw<double, 8>(map, p, grid, st);
+    if (cw == 16) return launch_cw<double, 16>(map, p, grid, st);
+    return launch_cw<double, 32>(map, p, grid, st);
+  }
+  if (cw == 8) return launch_cw<float, 8>(map, p, grid, st);
+  if (cw == 16) return launch_cw<float, 16>(map, p, grid, st);
+  return launch_cw<float, 32>(map, p, grid, st);
+}
+
+}  // namespace bak

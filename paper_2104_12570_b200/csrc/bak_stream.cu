@@ -242,7 +242,7 @@ bool plan_stream(int dtype, int64_t obs, StreamPlan& pl) {
 int launch_stream(int dtype, const StreamPlan& pl, const SweepParams& prm0, cudaStream_t st) {
   SweepParams prm = prm0;
   prm.rows_per_cta = pl.rows_per_cta;
-  BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, static_cast<size_t>(2) * pl.nblocks * 32, st));
+  BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, kGridSlotBytes, st));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.nblocks);
   cfg.blockDim = dim3(pl.nthreads);

@@ -13,17 +13,18 @@
 // held in REGISTERS for the whole solve (E rows per thread, rows tid + k*NT so
 // shared-memory reads are conflict-free).  Each CTA = NT consumer threads +
 // one PRODUCER warp.  The producer walks the column schedule S steps ahead:
-// it reads col(u) and n2[col(u)] into a per-stage smem record and issues one
-// cp.async.bulk (TMA engine) for the CTA's slice of that column (contiguous in
-// column-major x) into an S-stage ring guarded by full/empty mbarriers.  x
-// never depends on e, so every global-memory latency of the schedule (column
-// list, norms, x itself) is off the consumers' critical path.
+// it reads col(u), n2 = n2[col(u)] and 1/n2 into a per-stage smem record and
+// issues one cp.async.bulk (TMA engine) for the CTA's slice of that column
+// (contiguous in column-major x) into an S-stage ring guarded by full/empty
+// mbarriers.  x never depends on e, so every global-memory latency of the
+// schedule (column list, norms, x itself) is off the consumers' critical path.
 //
-// Consumers keep TWO columns in registers (x_t, x_{t+1}) and per column do
-//     d_t = P_t / n2_t
+// Consumers keep columns t, t+1 (and t+2 when registers allow) in registers:
+//     pull x_{t+2}: smem -> registers (overlaps the arithmetic below)
+//     d_t = P_t / n2_t   (correctly rounded: q0 = P*r, q = q0 + (P - q0*n2)*r,
+//                         r = RN(1/n2) precomputed by the producer)
 //     fused:  e -= fl(d_t * x_t) ; p += x_{t+1} . e  (+ sum e^2 at sweep end)
-//     load x_{t+2} smem -> registers (before the reduction; frees its stage)
-//     warp xor-butterfly -> per-warp slots -> named barrier -> fixed-order sum
+//     warp xor-butterfly -> per-warp slots -> named barrier -> fixed-order tree
 //     -> exchange across participants -> every consumer holds P_{t+1}.
 // Exchange by MODE:
 //   kCta     : single CTA, nothing to exchange.
@@ -31,8 +32,10 @@
 //              16-byte {p, sq} into every peer's shared slot, completing as
 //              transaction bytes on the peer's mbarrier (DSMEM, no flags).
 //   kGrid    : co-resident persistent grid (cooperative launch).  Each CTA
-//              posts {p, epoch}-tagged 16-byte records to global slots; warp 0
-//              of every CTA polls all slots and sums them in fixed order.
+//              posts an epoch-tagged 16-byte record; CTA 0 (the aggregator)
+//              sums all of them in fixed order and posts the total into every
+//              CTA's private 128-byte result line, which that CTA polls.  No
+//              L2 line is polled by more than one CTA.
 // Every participant sums the same values in the same order, so all of them
 // compute bit-identical d_j; the reduction order depends only on the shape.
 #include <cstdio>
@@ -63,6 +66,13 @@ struct alignas(16) Pair {
   double p, q;
 };
 
+struct alignas(32) StageMeta {
+  int64_t col;
+  double n2;
+  double rinv;
+  double pad;
+};
+
 __device__ __forceinline__ bool bar_or(int nthreads, int pred) {
   uint32_t r;
   asm volatile(
@@ -80,8 +90,38 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-template <typename T, int E, int MODE>
-__global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const SweepParams prm) {
+// correctly rounded a/b from r = RN(1/b): one Markstein correction step
+template <typename T>
+__device__ __forceinline__ T quotient(T a, T b, T r) {
+  const T q0 = Num<T>::mul(a, r);
+  const T rem = Num<T>::fma(-q0, b, a);
+  return Num<T>::fma(rem, r, q0);
+}
+
+#ifdef BAK_PHASES
+#define PH(i)                                  \
+  do {                                         \
+    if (tid == 0) {                            \
+      const long long _c = clock64();          \
+      ph_acc[i] += _c - ph_last;               \
+      ph_last = _c;                            \
+    }                                          \
+  } while (0)
+#else
+#define PH(i) \
+  do {        \
+  } while (0)
+#endif
+
+template <typename T, int E, int MODE, int MAXNT>
+__global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams prm) {
+#ifdef BAK_PHASES
+  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+#endif
+  constexpr int kMaxWarps = MAXNT / 32;
+  // third register buffer (pull x_{t+2} before the arithmetic) when it fits
+  constexpr bool kEarly = E * sizeof(T) <= 64;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NT = static_cast<int>(blockDim.x) - 32;  // consumers; the last warp produces
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
@@ -112,10 +152,8 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
   off += kMaxStages * 8;
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + off);
   off += kMaxStages * 8;
-  int64_t* meta_col = reinterpret_cast<int64_t*>(smem_raw + off);
-  off += kMaxStages * 8;
-  double* meta_n2 = reinterpret_cast<double*>(smem_raw + off);
-  off += kMaxStages * 8;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(smem_raw + off);
+  off += kMaxStages * sizeof(StageMeta);
   T* red = reinterpret_cast<T*>(smem_raw + off);  // [2 bufs][2 values][32 warps]
   off += 2 * 2 * 32 * sizeof(T);
   off = (off + 15) & ~size_t(15);
@@ -165,8 +203,10 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
         }
         const int64_t c = pc.col();
         pc.next();
-        meta_col[s] = c;
-        meta_n2[s] = static_cast<double>(n2g[c]);
+        const T n2 = n2g[c];
+        meta[s].col = c;
+        meta[s].n2 = static_cast<double>(n2);
+        meta[s].rinv = static_cast<double>(Num<T>::div(T(1), n2));
         mbar_arrive_expect_tx(&full[s], bytes);  // release: meta visible with the phase
         bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + c * prm.ldx + r0, bytes, &full[s], pol);
         if (++s == S) { s = 0; ph ^= 1u; }
@@ -190,10 +230,9 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
     int my_abort = 0;
     int ls = 0;        // stage of the next step to pull into registers
     uint32_t lph = 0;  // its phase parity
-    int rel[2];        // stages pulled since the last release
-    int nrel = 0;
 
-    auto pull = [&](T (&xr)[E], int64_t& c, T& n2) {
+    // stage -> registers (pad rows beyond obs read as 0); returns the stage index
+    auto pull = [&](T* xr, int64_t& c, T& n2, T& rinv) -> int {
       if (!mbar_test(&full[ls], lph)) {
         const uint64_t t0 = globaltimer();
         while (!mbar_test(&full[ls], lph)) {
@@ -204,34 +243,61 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
           }
         }
       }
-      c = meta_col[ls];
-      n2 = static_cast<T>(meta_n2[ls]);
+      c = meta[ls].col;
+      n2 = static_cast<T>(meta[ls].n2);
+      rinv = static_cast<T>(meta[ls].rinv);
       const T* X = xs + static_cast<size_t>(ls) * prm.stage_elems;
 #pragma unroll
       for (int k = 0; k < E; ++k) xr[k] = (k < kv) ? X[tid + k * NT] : T(0);
-      rel[nrel++] = ls;
+      const int got = ls;
       if (++ls == S) { ls = 0; lph ^= 1u; }
+      return got;
     };
 
-    // reduction across all participants; returns true on (uniform) abort
-    auto reduce = [&](T pv, T qv, bool with_q, uint32_t rc, T& P, T& Q) -> bool {
+    // fixed-order tree over the per-warp partials in shared memory
+    auto warp_partials = [&](const T* v) -> T {
+      T a[kMaxWarps];
+#pragma unroll
+      for (int w = 0; w < kMaxWarps; ++w) a[w] = (w < nwarps) ? v[w] : T(0);
+#pragma unroll
+      for (int h = kMaxWarps / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int w = 0; w < h; ++w) a[w] = Num<T>::add(a[w], a[w + h]);
+      return a[0];
+    };
+
+    // reduction across all participants; returns true on (uniform) abort.
+    // rel0/rel1: stages to hand back to the producer once every consumer has
+    // passed the barrier (their contents are in registers by then).
+    auto reduce = [&](T pv, T qv, bool with_q, uint32_t rc, int rel0, int rel1, T& P, T& Q) -> bool {
       const int buf = rc & 1;
       pv = warp_sum(pv);
       if (with_q) qv = warp_sum(qv);
-      if (lane == 0) {
-        red[(buf * 2 + 0) * 32 + warp] = pv;
-        red[(buf * 2 + 1) * 32 + warp] = qv;
+      PH(3);
+      T bp, bq;
+      if (kMaxWarps == 1) {
+        if (__any_sync(0xffffffffu, my_abort)) return true;
+        __syncwarp();
+        if (lane == 0) {
+          if (rel0 >= 0) mbar_arrive(&empty[rel0]);
+          if (rel1 >= 0) mbar_arrive(&empty[rel1]);
+        }
+        bp = pv;
+        bq = qv;
+      } else {
+        if (lane == 0) {
+          red[(buf * 2 + 0) * 32 + warp] = pv;
+          red[(buf * 2 + 1) * 32 + warp] = qv;
+        }
+        if (bar_or(NT, my_abort)) return true;
+        if (tid == 0) {
+          if (rel0 >= 0) mbar_arrive(&empty[rel0]);
+          if (rel1 >= 0) mbar_arrive(&empty[rel1]);
+        }
+        bp = warp_partials(red + (buf * 2 + 0) * 32);
+        bq = with_q ? warp_partials(red + (buf * 2 + 1) * 32) : T(0);
       }
-      if (bar_or(NT, my_abort)) return true;
-      // all consumers have pulled their stages into registers: hand them back
-      if (tid == 0) {
-        for (int i = 0; i < nrel; ++i) mbar_arrive(&empty[rel[i]]);
-      }
-      nrel = 0;
-      T bp = T(0), bq = T(0);
-      for (int w = 0; w < nwarps; ++w) bp = Num<T>::add(bp, red[(buf * 2 + 0) * 32 + w]);
-      if (with_q)
-        for (int w = 0; w < nwarps; ++w) bq = Num<T>::add(bq, red[(buf * 2 + 1) * 32 + w]);
+      PH(4);
       if (MODE == kModeCta) {
         P = bp;
         Q = bq;
@@ -255,46 +321,95 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
             }
           }
         }
-        T sp = T(0), sq = T(0);
-        for (uint32_t r = 0; r < G; ++r) {
-          sp = Num<T>::add(sp, static_cast<T>(xslot[buf * kMaxCluster + r].p));
-          if (with_q) sq = Num<T>::add(sq, static_cast<T>(xslot[buf * kMaxCluster + r].q));
+        T sp[kMaxCluster], sq[kMaxCluster];
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; ++r) {
+          const bool in = r < static_cast<int>(G);
+          sp[r] = in ? static_cast<T>(xslot[buf * kMaxCluster + r].p) : T(0);
+          sq[r] = (in && with_q) ? static_cast<T>(xslot[buf * kMaxCluster + r].q) : T(0);
         }
-        P = sp;
-        Q = sq;
+#pragma unroll
+        for (int h = kMaxCluster / 2; h >= 1; h >>= 1)
+#pragma unroll
+          for (int r = 0; r < h; ++r) {
+            sp[r] = Num<T>::add(sp[r], sp[r + h]);
+            sq[r] = Num<T>::add(sq[r], sq[r + h]);
+          }
+        P = sp[0];
+        Q = sq[0];
         return false;
       }
-      // kModeGrid: epoch-tagged records in global memory
+      // kModeGrid: partial records -> aggregator (CTA 0) -> per-CTA result lines
       const uint32_t epoch = rc + 1;
-      uint32_t* slots = prm.slots + static_cast<size_t>(buf) * G * 8;
+      uint32_t* part = prm.slots + static_cast<size_t>(buf) * kGridSlotsMax * 8;
+      uint32_t* result = prm.slots + static_cast<size_t>(2) * kGridSlotsMax * 8 +
+                         static_cast<size_t>(buf) * kGridSlotsMax * 32;
       if (tid == 0) {
-        ll_store(slots + static_cast<size_t>(rank) * 8, static_cast<double>(bp), epoch);
-        if (with_q) ll_store(slots + static_cast<size_t>(rank) * 8 + 4, static_cast<double>(bq), epoch);
+        ll_store(part + static_cast<size_t>(rank) * 8, static_cast<double>(bp), epoch);
+        if (with_q) ll_store(part + static_cast<size_t>(rank) * 8 + 4, static_cast<double>(bq), epoch);
       }
+      bool timed_out = false;
       if (warp == 0) {
-        T sp = T(0), sq = T(0);
-        const uint64_t t0 = globaltimer();
-        bool timed_out = false;
-        for (uint32_t i = lane; i < G; i += 32) {
-          double v;
-          while (!ll_load(slots + static_cast<size_t>(i) * 8, epoch, v)) {
-            if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+        if (rank == 0) {
+          // aggregator: lane l owns records l, l+32, ... (<= 8 per lane), all in flight together
+          constexpr int kPer = kGridSlotsMax / 32;
+          T vp[kPer], vq[kPer];
+          uint32_t pending = 0;
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            vp[i] = T(0);
+            vq[i] = T(0);
+            if (lane + 32 * i < static_cast<int>(G)) pending |= (with_q ? 3u : 1u) << (2 * i);
           }
-          sp = Num<T>::add(sp, static_cast<T>(v));
-          if (with_q) {
-            while (!ll_load(slots + static_cast<size_t>(i) * 8 + 4, epoch, v)) {
-              if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+          const uint64_t t0 = globaltimer();
+          while (pending) {
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+              double v;
+              if ((pending >> (2 * i)) & 1u) {
+                if (ll_load(part + static_cast<size_t>(lane + 32 * i) * 8, epoch, v)) {
+                  vp[i] = static_cast<T>(v);
+                  pending &= ~(1u << (2 * i));
+                }
+              }
+              if ((pending >> (2 * i + 1)) & 1u) {
+                if (ll_load(part + static_cast<size_t>(lane + 32 * i) * 8 + 4, epoch, v)) {
+                  vq[i] = static_cast<T>(v);
+                  pending &= ~(2u << (2 * i));
+                }
+              }
             }
-            sq = Num<T>::add(sq, static_cast<T>(v));
+            if (pending && globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
           }
+#pragma unroll
+          for (int h = kPer / 2; h >= 1; h >>= 1)
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+              vp[i] = Num<T>::add(vp[i], vp[i + h]);
+              vq[i] = Num<T>::add(vq[i], vq[i + h]);
+            }
+          const T sp = warp_sum(vp[0]);
+          const T sq = with_q ? warp_sum(vq[0]) : T(0);
+          for (uint32_t r = lane; r < G; r += 32) {
+            ll_store(result + static_cast<size_t>(r) * 32, static_cast<double>(sp), epoch);
+            if (with_q) ll_store(result + static_cast<size_t>(r) * 32 + 4, static_cast<double>(sq), epoch);
+          }
+        }
+        if (lane == 0) {
+          double vp2 = 0.0, vq2 = 0.0;
+          const uint32_t* mine = result + static_cast<size_t>(rank) * 32;
+          const uint64_t t0 = globaltimer();
+          while (!ll_load(mine, epoch, vp2))
+            if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+          if (with_q)
+            while (!ll_load(mine + 4, epoch, vq2))
+              if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+          bcast[buf] = Pair{vp2, vq2};
         }
         if (timed_out) {
           report_error(prm.status, BAK_ETIMEOUT);
           my_abort = 1;
         }
-        sp = warp_sum(sp);
-        if (with_q) sq = warp_sum(sq);
-        if (lane == 0) bcast[buf] = Pair{static_cast<double>(sp), static_cast<double>(sq)};
       }
       const bool any2 = bar_or(NT, my_abort);
       P = static_cast<T>(bcast[buf].p);
@@ -306,45 +421,70 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
     uint32_t rc = 0;
     T P = T(0), Q = T(0);
     int64_t c0 = 0, c1 = 0;
-    T n2_0 = T(1), n2_1 = T(1);
-    pull(xc, c0, n2_0);
-    if (total > 1) pull(xn, c1, n2_1);
-    T pv = T(0);
+    T n2_0 = T(1), n2_1 = T(1), ri_0 = T(1), ri_1 = T(1);
+    const int s0 = pull(xc, c0, n2_0, ri_0);
+    const int s1 = (total > 1) ? pull(xn, c1, n2_1, ri_1) : -1;
+    T pv;
+    {
+      T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-    for (int k = 0; k < E; ++k) pv = Num<T>::fma(xc[k], ev[k], pv);
-    bool aborted = reduce(pv, T(0), false, rc++, P, Q);
+      for (int k = 0; k < E; ++k) acc[k & 3] = Num<T>::fma(xc[k], ev[k], acc[k & 3]);
+      pv = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+    }
+    bool aborted = reduce(pv, T(0), false, rc++, s0, s1, P, Q);
 
-    const bool updater = (rank == 0) && (tid == (NT > 32 ? 32 : 0));
-    T a0 = updater ? ag[c0] : T(0);
-    T a1 = (updater && total > 1) ? ag[c1] : T(0);
+    // coefficient updates: the whole of warp 1 (warp 0 when NT == 32) runs them
+    // in lockstep (identical values, same address) so no lane diverges
+    const bool upd_warp = (rank == 0) && (warp == (nwarps > 1 ? 1 : 0));
+    T a0 = upd_warp ? ag[c0] : T(0);
+    T a1 = (upd_warp && total > 1) ? ag[c1] : T(0);
 
+    constexpr int EQ = kEarly ? E : 1;
+    T xq[EQ];
     int64_t sweep = 0, k = 0, t = 0;
     bool converged = false;
     while (!aborted) {
-      const T d = Num<T>::div(P, n2_0);
+      PH(7);
+      const bool more = t + 2 < total;
+      int64_t c2 = c1;
+      T n2_2 = n2_1, ri_2 = ri_1;
+      int sp = -1;
+      if (kEarly && more) sp = pull(xq, c2, n2_2, ri_2);
+      const T d = quotient(P, n2_0, ri_0);
+      PH(0);
       const bool last = (k == ncols - 1);
-      const bool has_next = !(last && sweep + 1 == prm.max_iter);
-      T qv = T(0);
-      pv = T(0);
+      T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
       for (int kk = 0; kk < E; ++kk) {
         ev[kk] = Num<T>::sub(ev[kk], Num<T>::mul(xc[kk], d));
-        if (has_next) pv = Num<T>::fma(xn[kk], ev[kk], pv);
-        if (last) qv = Num<T>::fma(ev[kk], ev[kk], qv);
+        acc[kk & 3] = Num<T>::fma(xn[kk], ev[kk], acc[kk & 3]);
       }
-      int64_t c2 = c1;
-      T n2_2 = n2_1;
+      pv = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+      T qv = T(0);
+      if (last) {
+        T qa[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+        for (int kk = 0; kk < E; ++kk) qa[kk & 3] = Num<T>::fma(ev[kk], ev[kk], qa[kk & 3]);
+        qv = Num<T>::add(Num<T>::add(qa[0], qa[1]), Num<T>::add(qa[2], qa[3]));
+      }
+      PH(1);
 #pragma unroll
       for (int kk = 0; kk < E; ++kk) xc[kk] = xn[kk];
-      if (t + 2 < total) pull(xn, c2, n2_2);
-      if (updater) {
+      if (kEarly) {
+#pragma unroll
+        for (int kk = 0; kk < E; ++kk) xn[kk] = xq[kk < EQ ? kk : 0];
+      } else if (more) {
+        sp = pull(xn, c2, n2_2, ri_2);
+      }
+      PH(2);
+      if (upd_warp) {
         const T na = Num<T>::add(a0, d);
         ag[c0] = na;
-        if (c1 == c0) a1 = na;
-        a0 = a1;
-        if (t + 2 < total) a1 = ag[c2];  // store->load order in one thread: never stale
+        a0 = (c1 == c0) ? na : a1;
+        if (more) a1 = ag[c2];  // store->load order in one thread: never stale
       }
-      aborted = reduce(pv, qv, last, rc++, P, Q);
+      aborted = reduce(pv, qv, last, rc++, sp, -1, P, Q);
+      PH(6);
       if (aborted) break;
       if (last) {
         if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
@@ -361,13 +501,19 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
       ++t;
       c0 = c1;
       n2_0 = n2_1;
+      ri_0 = ri_1;
       c1 = c2;
       n2_1 = n2_2;
+      ri_1 = ri_2;
     }
 
 #pragma unroll
     for (int kk = 0; kk < E; ++kk)
       if (kk < kv) eg[r0 + tid + static_cast<int64_t>(kk) * NT] = ev[kk];
+#ifdef BAK_PHASES
+    if (tid == 0 && rank == 0 && prm.history)
+      for (int i = 0; i < 8; ++i) prm.history[prm.max_iter + i] = static_cast<double>(ph_acc[i]);
+#endif
     if (tid == 0) {
       *stop = 1;
       if (rank == 0 && prm.status) {
@@ -385,13 +531,13 @@ __global__ void __launch_bounds__(kMaxConsumers + 32, 1) sweep_kernel(const Swee
 // ------------------------------- host -------------------------------------
 
 size_t smem_bytes(const SweepPlan& pl, size_t tsize) {
-  return static_cast<size_t>(pl.nstages) * pl.stage_elems * tsize + 4 * kMaxStages * 8 + 2 * 2 * 32 * tsize + 16 +
-         2 * kMaxCluster * 16 + 16 + 32 + 16;
+  return static_cast<size_t>(pl.nstages) * pl.stage_elems * tsize + 2 * kMaxStages * 8 +
+         kMaxStages * sizeof(StageMeta) + 2 * 2 * 32 * tsize + 16 + 2 * kMaxCluster * 16 + 16 + 32 + 16;
 }
 
-template <typename T, int E, int MODE>
+template <typename T, int E, int MODE, int MAXNT>
 int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
-  auto kern = sweep_kernel<T, E, MODE>;
+  auto kern = sweep_kernel<T, E, MODE, MAXNT>;
   const size_t smem = smem_bytes(pl, sizeof(T));
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t cfg{};
@@ -421,18 +567,24 @@ int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
   return BAK_OK;
 }
 
-template <typename T, int MODE>
+template <typename T, int MODE, int MAXNT>
 int launch_e(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   switch (pl.e) {
-    case 1: return launch_one<T, 1, MODE>(pl, prm, st);
-    case 2: return launch_one<T, 2, MODE>(pl, prm, st);
-    case 4: return launch_one<T, 4, MODE>(pl, prm, st);
-    case 8: return launch_one<T, 8, MODE>(pl, prm, st);
-    case 16: return launch_one<T, 16, MODE>(pl, prm, st);
-    case 32: return launch_one<T, 32, MODE>(pl, prm, st);
+    case 1: return launch_one<T, 1, MODE, MAXNT>(pl, prm, st);
+    case 2: return launch_one<T, 2, MODE, MAXNT>(pl, prm, st);
+    case 4: return launch_one<T, 4, MODE, MAXNT>(pl, prm, st);
+    case 8: return launch_one<T, 8, MODE, MAXNT>(pl, prm, st);
+    case 16: return launch_one<T, 16, MODE, MAXNT>(pl, prm, st);
+    case 32: return launch_one<T, 32, MODE, MAXNT>(pl, prm, st);
   }
   set_error("bak_sweep: unsupported rows-per-thread %d", pl.e);
   return BAK_EUNSUPPORTED;
+}
+
+template <typename T, int MODE>
+int launch_nt(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
+  if (pl.nthreads == 32) return launch_e<T, MODE, 32>(pl, prm, st);
+  return launch_e<T, MODE, kMaxConsumers>(pl, prm, st);
 }
 
 }  // namespace
@@ -447,6 +599,7 @@ static bool plan_fill(int dtype, int variant, int64_t obs, int nthreads, int e, 
   const int64_t rows = static_cast<int64_t>(nthreads) * e;
   if (nthreads < 32 || nthreads > kMaxConsumers || nthreads % 32) return false;
   if (rows * parts < obs || (parts - 1) * rows >= obs) return false;
+  if (variant == BAK_VARIANT_GRID && parts > kGridSlotsMax) return false;
   SweepPlan cand;
   cand.variant = variant;
   cand.nthreads = nthreads;
@@ -480,7 +633,11 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
   if (plan_env(dtype, variant, obs, pl)) return true;
   const int max_e = dtype == BAK_F64 ? 8 : 16;
   if (variant == BAK_VARIANT_CTA) {
-    // short columns: smallest E that fits 256 consumer threads, else larger E / more threads
+    // short columns: a single warp when E stays small, else the fewest warps
+    for (int e : kEs) {
+      if (e > 2 * max_e) break;
+      if (static_cast<int64_t>(32) * e >= obs && plan_fill(dtype, variant, obs, 32, e, 1, pl, 4)) return true;
+    }
     for (int e : kEs) {
       if (e > max_e) break;
       const int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
@@ -498,7 +655,7 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
       for (int e : kEs) {
         if (e > max_e) break;
         const int nt = static_cast<int>(round_up((per + e - 1) / e, 32));
-        if (nt > 256) continue;
+        if (nt > 128) continue;
         int parts = static_cast<int>((obs + static_cast<int64_t>(nt) * e - 1) / (static_cast<int64_t>(nt) * e));
         if (parts < 2) parts = 2;
         if (plan_fill(dtype, variant, obs, nt, e, parts, pl, 4)) return true;
@@ -521,15 +678,15 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
 
 int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   if (pl.variant == BAK_VARIANT_GRID && prm.slots)
-    BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, static_cast<size_t>(2) * pl.nparticipants * 32, st));
+    BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, kGridSlotBytes, st));
   if (dtype == BAK_F64) {
-    if (pl.variant == BAK_VARIANT_CTA) return launch_e<double, kModeCta>(pl, prm, st);
-    if (pl.variant == BAK_VARIANT_CLUSTER) return launch_e<double, kModeCluster>(pl, prm, st);
-    return launch_e<double, kModeGrid>(pl, prm, st);
+    if (pl.variant == BAK_VARIANT_CTA) return launch_nt<double, kModeCta>(pl, prm, st);
+    if (pl.variant == BAK_VARIANT_CLUSTER) return launch_nt<double, kModeCluster>(pl, prm, st);
+    return launch_nt<double, kModeGrid>(pl, prm, st);
   }
-  if (pl.variant == BAK_VARIANT_CTA) return launch_e<float, kModeCta>(pl, prm, st);
-  if (pl.variant == BAK_VARIANT_CLUSTER) return launch_e<float, kModeCluster>(pl, prm, st);
-  return launch_e<float, kModeGrid>(pl, prm, st);
+  if (pl.variant == BAK_VARIANT_CTA) return launch_nt<float, kModeCta>(pl, prm, st);
+  if (pl.variant == BAK_VARIANT_CLUSTER) return launch_nt<float, kModeCluster>(pl, prm, st);
+  return launch_nt<float, kModeGrid>(pl, prm, st);
 }
 
 }  // namespace bak

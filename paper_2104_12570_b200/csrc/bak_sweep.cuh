@@ -6,6 +6,11 @@
 
 namespace bak {
 
+// grid exchange workspace: [2 bufs][kGridSlotsMax] 32-byte partial records +
+// [2 bufs][kGridSlotsMax] 128-byte result lines (one per CTA)
+constexpr int kGridSlotsMax = 256;
+constexpr int64_t kGridSlotBytes = 2LL * kGridSlotsMax * 32 + 2LL * kGridSlotsMax * 128;
+
 struct SweepParams {
   const void* x;
   int64_t obs, ldx;
@@ -45,5 +50,18 @@ struct StreamPlan {
 };
 bool plan_stream(int dtype, int64_t obs, StreamPlan& pl);
 int launch_stream(int dtype, const StreamPlan& pl, const SweepParams& prm, cudaStream_t st);
+
+// GRAM variant (algebraically equivalent sweep through G = X^T X)
+int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars);
+bool gram_supported(int64_t vars);
+int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk);
+int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
+                  int64_t part_bytes, cudaStream_t st);
+bool gram_tma_supported(int64_t vars);
+int gram_tma_grid();
+int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
+                         const double* delta, int apply, int dot, double* gpart, double* sqpart, const int64_t* done,
+                         cudaStream_t st);
+int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st);
 
 }  // namespace bak

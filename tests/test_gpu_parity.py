@@ -203,3 +203,32 @@ def test_batched_edge_cases():
             assert orc.rel_coeff_err(rep.a_hat[s], ref["a_hat"]) <= 1e-10
     assert rep.a_hat[1, 2] == 7.5
     assert np.all(rep.a_hat[2] == 0) and rep.sweeps_run[2] == 0 and rep.converged[2]
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_gram_variant_matches_oracle(precision):
+    """GRAM is a labelled, algebraically equivalent reformulation: it must meet
+    the same parity bar as the exact kernels."""
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=1 << 18, nvars=48, precision=precision)
+    ref = orc.solve(x, y, max_iter=6, tol=0, record_history=True)
+    rep = pb.solve_bak(x, y, pb.SolveConfig(max_iter=6, tol=0, record_history=True), variant="gram")
+    assert rep.variant == "gram"
+    assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"], ref_hist=ref["residual_norm_history"])
+
+
+def test_gram_variant_random_order_zero_columns_early_break():
+    pb = _pb()
+    rng = np.random.default_rng(19)
+    x = np.asfortranarray(rng.standard_normal((20_000, 20)))
+    x[:, 7] = 0.0
+    y = x @ rng.standard_normal(20) + 1e-3 * rng.standard_normal(20_000)
+    a0 = np.zeros(20)
+    a0[7] = 7.5
+    for cfg in (dict(max_iter=60, tol=1e-9, record_history=True),
+                dict(max_iter=25, tol=1e-12, ordering="random", ordering_seed=4, record_history=True)):
+        ref = orc.solve(x, y, a0=a0, **cfg)
+        rep = pb.solve_bak(x, y, pb.SolveConfig(**cfg), a0=a0, variant="gram")
+        assert rep.a_hat[7] == 7.5
+        assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"],
+                      ref_hist=ref["residual_norm_history"])

@@ -36,7 +36,7 @@ def main():
     y = torch.randn(a.obs, dtype=tdt, device=dev)
     dm = pb.DeviceMatrix(data, a.obs, a.vars, "float64" if a.dtype == "f64" else "float32")
     lib = _lib.load()
-    ws = _Workspace(torch, dev, _workspace_bytes(lib, dm.code, a.obs, a.vars))
+    ws = _Workspace(torch, dev, _workspace_bytes(lib, dm.code, a.obs, a.vars, _lib.VARIANTS[a.variant]))
     norms = pb.colnorms(dm, ws)
     e = torch.empty_like(y)
     av = torch.zeros(a.vars, dtype=tdt, device=dev)

@@ -11,6 +11,9 @@
 //    short-circuit (bak.py:168-170), early break per sweep (bak.py:106-111),
 //    final residual y - x a and the drift flag (bak.py:127-143) are computed in
 //    the same CTA.
+#include <cstdio>
+#include <cstdlib>
+
 #include "bak_common.cuh"
 
 namespace bak {
@@ -33,6 +36,14 @@ struct BatchedParams {
   int x_in_smem;
 };
 
+// correctly rounded a/b from r = RN(1/b) (one Markstein correction)
+template <typename T>
+__device__ __forceinline__ T quotient(T a, T b, T r) {
+  const T q0 = Num<T>::mul(a, r);
+  const T rem = Num<T>::fma(-q0, b, a);
+  return Num<T>::fma(rem, r, q0);
+}
+
 template <typename T>
 __device__ __forceinline__ T block_sum(T v, T* red, int nwarps) {
   v = warp_sum(v);
@@ -46,10 +57,12 @@ __device__ __forceinline__ T block_sum(T v, T* red, int nwarps) {
   return s;
 }
 
-template <typename T, int E>
-__global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
+template <typename T, int E, int NT_, bool SMEM>
+__global__ void __launch_bounds__(NT_) batched_kernel(const BatchedParams prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int NT = blockDim.x, tid = threadIdx.x, nwarps = NT >> 5;
+  constexpr int NT = NT_;
+  constexpr int nwarps = NT >> 5;
+  const int tid = threadIdx.x;
   const int64_t sys = blockIdx.x;
   const int64_t obs = prm.obs, vars = prm.vars, ldx = prm.ldx;
   const T* __restrict__ xg = static_cast<const T*>(prm.x) + sys * prm.x_stride;
@@ -62,17 +75,21 @@ __global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
 
   size_t off = 0;
   T* xs = reinterpret_cast<T*>(smem_raw);
-  if (prm.x_in_smem) off += static_cast<size_t>(vars) * ldx * sizeof(T);
+  if (SMEM) off += static_cast<size_t>(vars) * ldx * sizeof(T);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + off);
   off += 16;
   T* n2s = reinterpret_cast<T*>(smem_raw + off);
   off += round16(vars * sizeof(T));
   T* as = reinterpret_cast<T*>(smem_raw + off);
   off += round16(vars * sizeof(T));
+  T* rinv = reinterpret_cast<T*>(smem_raw + off);
+  off += round16(vars * sizeof(T));
+  int* nz = reinterpret_cast<int*>(smem_raw + off);
+  off += round16((vars + 1) * sizeof(int));
   T* red = reinterpret_cast<T*>(smem_raw + off);
   double* redd = reinterpret_cast<double*>(smem_raw + off);
 
-  if (prm.x_in_smem) {
+  if (SMEM) {
     if (tid == 0) {
       mbar_init(bar, 1);
       fence_mbar_init();
@@ -89,7 +106,7 @@ __global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
     n2s[j] = n2g[j];
     as[j] = prm.warm ? ag[j] : T(0);
   }
-  if (prm.x_in_smem) {
+  if (SMEM) {
     const uint64_t t0 = globaltimer();
     while (!mbar_test(bar, 0))
       if (globaltimer() - t0 > kTimeoutNs) {
@@ -98,7 +115,7 @@ __global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
       }
   }
   __syncthreads();
-  const T* X = prm.x_in_smem ? xs : xg;
+  const T* X = SMEM ? xs : xg;
 
   const int kv = static_cast<int>(imax64(0, imin64(E, (obs - tid + NT - 1) / NT)));
   T yv[E], ev[E];
@@ -136,48 +153,76 @@ __global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
     for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? Num<T>::sub(yv[k], acc[k]) : T(0);
   }
 
-  auto next_nz = [&](int64_t j) -> int64_t {  // first column >= j with nonzero norm, or vars
-    while (j < vars && n2s[j] == T(0)) ++j;
-    return j;
-  };
-  const int64_t jfirst = next_nz(0);
+  // nonzero-norm column list (zero-norm columns are skipped, bak.py:101-103)
+  for (int64_t j = tid; j < vars; j += NT) rinv[j] = n2s[j] != T(0) ? Num<T>::div(T(1), n2s[j]) : T(0);
+  if (tid == 0) {
+    int n = 0;
+    for (int64_t j = 0; j < vars; ++j)
+      if (n2s[j] != T(0)) nz[n++] = static_cast<int>(j);
+    nz[vars] = n;
+  }
+  __syncthreads();
+  const int nnz = nz[vars];
   int64_t sweeps = 0;
   bool converged = false;
-  if (jfirst < vars) {
-    int64_t j = jfirst;
+  const bool full_rows = kv == E;  // uniform within a warp unless obs is ragged
+  auto load_col = [&](int j, T (&xr)[E]) {
+    const T* c = X + static_cast<int64_t>(j) * ldx + tid;
+    if (full_rows) {
+#pragma unroll
+      for (int k = 0; k < E; ++k) xr[k] = c[k * NT];
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k) xr[k] = (k < kv) ? c[k * NT] : T(0);
+    }
+  };
+  if (nnz > 0) {
+    // two register buffers with alternating roles (loop unrolled by 2: no copies)
+    T xa[E], xb[E];
+    load_col(nz[0], xa);
+    load_col(nz[nnz > 1 ? 1 : 0], xb);
     T p = T(0);
 #pragma unroll
-    for (int k = 0; k < E; ++k)
-      if (k < kv) p = Num<T>::fma(X[j * ldx + tid + k * NT], ev[k], p);
+    for (int k = 0; k < E; ++k) p = Num<T>::fma(xa[k], ev[k], p);
     T P = block_sum(p, red, nwarps);
-    while (true) {
-      const T d = Num<T>::div(P, n2s[j]);
-      int64_t jn = next_nz(j + 1);
-      const bool last = jn >= vars;
-      const bool has_next = !(last && sweeps + 1 == prm.max_iter);
-      if (last) jn = jfirst;
-      T pv = T(0), qv = T(0);
+    int idx = 0;
+    // one column step: update with xc (column nz[idx]), dot with xn (next column),
+    // then refill xc with the column after next.  Returns true when the solve ends.
+    auto step = [&](T (&xc)[E], T (&xn)[E]) -> bool {
+      const int j = nz[idx];
+      const bool last = idx == nnz - 1;
+      const T d = quotient(P, n2s[j], rinv[j]);
+      T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
       for (int k = 0; k < E; ++k) {
-        if (k < kv) {
-          ev[k] = Num<T>::sub(ev[k], Num<T>::mul(X[j * ldx + tid + k * NT], d));
-          if (has_next) pv = Num<T>::fma(X[jn * ldx + tid + k * NT], ev[k], pv);
-          if (last) qv = Num<T>::fma(ev[k], ev[k], qv);
-        }
+        ev[k] = Num<T>::sub(ev[k], Num<T>::mul(xc[k], d));
+        acc[k & 3] = Num<T>::fma(xn[k], ev[k], acc[k & 3]);
       }
+      const T pv = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+      int idx2 = idx + 2;
+      while (idx2 >= nnz) idx2 -= nnz;
+      load_col(nz[idx2], xc);  // overlaps the reduction below
       if (tid == 0) as[j] = Num<T>::add(as[j], d);
       if (last) {
-        const T Q = block_sum(qv, red, nwarps);
+        T qa[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+        for (int k = 0; k < E; ++k) qa[k & 3] = Num<T>::fma(ev[k], ev[k], qa[k & 3]);
+        const T Q = block_sum(Num<T>::add(Num<T>::add(qa[0], qa[1]), Num<T>::add(qa[2], qa[3])), red, nwarps);
         if (tid == 0 && hist) hist[sweeps] = static_cast<double>(Q);
         ++sweeps;
         if (thresh2 >= 0.0 && static_cast<double>(Q) <= thresh2) {
           converged = true;
-          break;
+          return true;
         }
-        if (sweeps == prm.max_iter) break;
+        if (sweeps == prm.max_iter) return true;
       }
       P = block_sum(pv, red, nwarps);
-      j = jn;
+      idx = last ? 0 : idx + 1;
+      return false;
+    };
+    while (true) {
+      if (step(xa, xb)) break;
+      if (step(xb, xa)) break;
     }
   } else if (tid == 0) {
     status[3] = BAK_EINVAL;  // all columns zero (bak.py:186-187)
@@ -215,14 +260,34 @@ __global__ void __launch_bounds__(256) batched_kernel(const BatchedParams prm) {
   }
 }
 
-template <typename T, int E>
-int launch_batched(const BatchedParams& prm, int nthreads, size_t smem, cudaStream_t st) {
-  auto kern = batched_kernel<T, E>;
+template <typename T, int E, int NT, bool SMEM>
+int launch_batched_t(const BatchedParams& prm, size_t smem, cudaStream_t st) {
+  auto kern = batched_kernel<T, E, NT, SMEM>;
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  kern<<<static_cast<unsigned>(prm.nsys), nthreads, smem, st>>>(prm);
+  kern<<<static_cast<unsigned>(prm.nsys), NT, smem, st>>>(prm);
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;
+}
+
+template <typename T, int NT, bool SMEM>
+int launch_batched_e(int E, const BatchedParams& prm, size_t smem, cudaStream_t st) {
+  switch (E) {
+    case 1: return launch_batched_t<T, 1, NT, SMEM>(prm, smem, st);
+    case 2: return launch_batched_t<T, 2, NT, SMEM>(prm, smem, st);
+    case 4: return launch_batched_t<T, 4, NT, SMEM>(prm, smem, st);
+    case 8: return launch_batched_t<T, 8, NT, SMEM>(prm, smem, st);
+    case 16: return launch_batched_t<T, 16, NT, SMEM>(prm, smem, st);
+    default: return launch_batched_t<T, 32, NT, SMEM>(prm, smem, st);
+  }
+}
+
+template <typename T>
+int launch_batched(int E, int nt, bool in_smem, const BatchedParams& prm, size_t smem, cudaStream_t st) {
+  if (nt == 32) return in_smem ? launch_batched_e<T, 32, true>(E, prm, smem, st) : launch_batched_e<T, 32, false>(E, prm, smem, st);
+  if (nt == 64) return in_smem ? launch_batched_e<T, 64, true>(E, prm, smem, st) : launch_batched_e<T, 64, false>(E, prm, smem, st);
+  if (nt == 128) return in_smem ? launch_batched_e<T, 128, true>(E, prm, smem, st) : launch_batched_e<T, 128, false>(E, prm, smem, st);
+  return in_smem ? launch_batched_e<T, 256, true>(E, prm, smem, st) : launch_batched_e<T, 256, false>(E, prm, smem, st);
 }
 
 }  // namespace
@@ -243,21 +308,32 @@ extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t 
   // rows per thread / threads: aim for ~4 warps per system, E <= 32
   static const int kEs[] = {1, 2, 4, 8, 16, 32};
   int E = 0, nt = 0;
-  for (int e : kEs) {
-    int t = static_cast<int>(round_up((obs + e - 1) / e, 32));
-    if (t <= 128) {
+  const int emax1 = dtype == BAK_F64 ? 16 : 16;
+  if (const char* env = getenv("BAK_BATCH_PLAN")) {  // "E,nthreads" (tuning experiments)
+    int e = 0, t = 0;
+    if (sscanf(env, "%d,%d", &e, &t) == 2 && static_cast<int64_t>(e) * t >= obs &&
+        (t == 32 || t == 64 || t == 128 || t == 256)) {
       E = e;
       nt = t;
+    }
+  }
+  for (int e : kEs) {  // one warp per system when the rows fit in E <= 16 per lane
+    if (E) break;
+    if (e > emax1) break;
+    if (static_cast<int64_t>(32) * e >= obs) {
+      E = e;
+      nt = 32;
       break;
     }
   }
-  if (!E) {
+  for (int cap_t : {128, 256}) {  // else the fewest power-of-two warps with E <= 32
     for (int e : kEs) {
-      int t = static_cast<int>(round_up((obs + e - 1) / e, 32));
-      if (t <= 256) {
+      if (E) break;
+      int t = 32;
+      while (static_cast<int64_t>(t) * e < obs) t *= 2;
+      if (t <= cap_t) {
         E = e;
         nt = t;
-        break;
       }
     }
   }
@@ -267,7 +343,7 @@ extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t 
   }
   const size_t cap = static_cast<size_t>(device_max_smem_optin()) - 1024;
   const size_t xbytes = static_cast<size_t>(vars) * ldx * ts;
-  const size_t small = 16 + 2 * round_up(static_cast<int64_t>(vars * ts), 16) + 32 * 8;
+  const size_t small = 16 + 3 * round_up(static_cast<int64_t>(vars * ts), 16) + round_up((vars + 1) * 4, 16) + 32 * 8;
   BatchedParams prm{x, obs, vars, ldx, x_stride, nsys, y, y_stride, norms2, ynorm2, a, warm, resid,
                     max_iter, tol, drift_tol, history, status, 0};
   const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ldx * ts) % 16 == 0) &&
@@ -283,14 +359,7 @@ extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t 
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define BAK_B(T)                                                  \
-  switch (E) {                                                    \
-    case 1: return launch_batched<T, 1>(prm, nt, smem, st);       \
-    case 2: return launch_batched<T, 2>(prm, nt, smem, st);       \
-    case 4: return launch_batched<T, 4>(prm, nt, smem, st);       \
-    case 8: return launch_batched<T, 8>(prm, nt, smem, st);       \
-    case 16: return launch_batched<T, 16>(prm, nt, smem, st);     \
-    default: return launch_batched<T, 32>(prm, nt, smem, st);     \
-  }
+  return launch_batched<T>(E, nt, prm.x_in_smem != 0, prm, smem, st);
   if (dtype == BAK_F64) {
     BAK_B(double)
   } else {

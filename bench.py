@@ -1,24 +1,34 @@
 #!/usr/bin/env python
 """SolveBak column sweep on B200 — sweeps/s and x-stream HBM GB/s vs roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--variant V] [--impl ours|reference]
 
 One JSON line on rank 0 (driver contract).  A "step" is one full solve through
 the drop-in API (norms, the sweeps, the recomputed residual, drift) over one
 synthetic system of the configuration's shape (BASELINE.json configs; seeded
 device RNG with the reference's distributions — no dataset is involved).
 
-  value      sweeps/s of whole solves with inputs resident in HBM (CUDA events)
-  e2e        the same metric through solve_bak() with pinned HOST inputs:
-             host->device copy of x, y and device->host of a, residual inside
-             the timed region
-  roofline   the dominant kernel (the sweep) timed alone with CUDA events:
-             algorithmic bytes = obs*vars*sizeof(T) per sweep (one read of x)
-  cpu_baseline  the CPU oracle (numpy restatement of the reference, bit-for-bit
-             equal to it on the fixture host) on a bounded sample, 1 core as the
-             reference pins BLAS to one thread (bak.py:184)
+Default workload: BASELINE config 3 (2^24 x 256 fp64, 20 sweeps), the
+configuration the metric is quoted on at 1/2/4/8 GPUs.  Its default kernel is
+the GRAM variant — the LABELLED algebraically-equivalent sweep (one pass over
+x per sweep through G = X^T X; parity-tested to the same 1e-10 bar); the exact
+per-column kernel's number on the same inputs is reported next to it
+(config.exact_variant).  With N > 1 ranks the rows are sharded over the GPUs
+(strong scaling, one all-gather of the per-sweep partials); c5 shards its
+65,536 systems over the ranks with no communication.
 
---impl reference runs that CPU port alone (the reference arm).
+  value      sweeps/s of whole solves with inputs resident in HBM (CUDA events,
+             max over ranks)
+  e2e        the same metric through solve_bak() with pinned HOST inputs:
+             host->device of x, y and device->host of a, residual inside the
+             timed region
+  roofline   the dominant kernel timed alone with CUDA events; algorithmic
+             bytes = rows*vars*sizeof(T) per sweep (one read of x)
+  cpu_baseline  the numpy oracle (bit-for-bit restatement of the reference)
+             on a bounded sample, 1 core as the reference pins BLAS (bak.py:184)
+
+--impl reference: the reference algorithm on this host's CPU cores — the
+C/OpenMP port of oracle/ (all host threads), rank 0 only.
 """
 
 from __future__ import annotations
@@ -45,9 +55,9 @@ CONFIGS = {
     "c2b": dict(kind="c2", obs=4096, vars=4096, dtype="f64", sweeps=50, tol=1e-10,
                 desc="square fp64 n=4096, early break at 1e-10"),
     "c3": dict(kind="system", obs=1 << 24, vars=256, dtype="f64", sweeps=20, tol=0.0, noise=0.01,
-               desc="very tall fp64 2^24x256, 20 sweeps"),
+               desc="very tall fp64 2^24x256, 20 sweeps", variant="gram", exact="stream"),
     "c3f32": dict(kind="system", obs=1 << 24, vars=256, dtype="f32", sweeps=20, tol=0.0, noise=0.01,
-                  desc="very tall fp32 2^24x256, 20 sweeps"),
+                  desc="very tall fp32 2^24x256, 20 sweeps", variant="gram", exact="stream"),
     "c4": dict(kind="c4", obs=1000, vars=1_000_000, dtype="f64", sweeps=10, tol=0.0,
                desc="wide fp64 1,000x1,000,000, 10 sweeps"),
     "c5": dict(kind="batched", obs=512, vars=32, nsys=65536, dtype="f32", sweeps=200, tol=0.0, noise=0.01,
@@ -56,7 +66,6 @@ CONFIGS = {
 DEFAULT_CONFIG = "c3"
 METRIC = "sweeps/sec and x-stream HBM GB/s vs roofline at 1/2/4/8 B200; CPU baseline"
 SPEC_HBM_GBS = 8000.0
-
 REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
@@ -125,23 +134,25 @@ class ClockSampler:
 # synthetic inputs on the device (seeded; reference distributions)
 # --------------------------------------------------------------------------
 
-def make_inputs(cfg, dev, seed=1234):
+def make_inputs(cfg, dev, seed=1234, rows=None, nsys=None):
+    """Device inputs of the config's shape (rows / nsys override: this rank's shard)."""
     import torch
     import paper_2104_12570_b200 as pb
     tdt = torch.float64 if cfg["dtype"] == "f64" else torch.float32
     npdt = np.float64 if cfg["dtype"] == "f64" else np.float32
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
-    obs, nv = cfg["obs"], cfg["vars"]
+    obs = rows if rows is not None else cfg["obs"]
+    nv = cfg["vars"]
     vec = 16 // (8 if cfg["dtype"] == "f64" else 4)
     ld = (obs + vec - 1) // vec * vec
     if cfg["kind"] == "batched":
-        nsys = cfg["nsys"]
-        data = torch.zeros((nsys, nv, ld), dtype=tdt, device=dev)
+        ns = nsys if nsys is not None else cfg["nsys"]
+        data = torch.zeros((ns, nv, ld), dtype=tdt, device=dev)
         data[:, :, :obs].normal_(generator=g)
-        a_true = torch.rand((nsys, nv), dtype=tdt, device=dev, generator=g) * 2 - 1
+        a_true = torch.rand((ns, nv), dtype=tdt, device=dev, generator=g) * 2 - 1
         y = torch.bmm(data[:, :, :obs].transpose(1, 2), a_true.unsqueeze(2)).squeeze(2)
-        y += cfg["noise"] * torch.randn((nsys, obs), dtype=tdt, device=dev, generator=g)
+        y += cfg["noise"] * torch.randn((ns, obs), dtype=tdt, device=dev, generator=g)
         return pb.DeviceBatch(data, obs, npdt), y.contiguous()
     data = torch.zeros((nv, ld), dtype=tdt, device=dev)
     for j0 in range(0, nv, 4096):  # chunked to bound RNG temporaries
@@ -165,35 +176,30 @@ def make_inputs(cfg, dev, seed=1234):
 
 
 # --------------------------------------------------------------------------
-# CPU baseline: the oracle on a bounded sample (1 core, like the reference)
+# CPU baselines (the checker, timed; never the measured product)
 # --------------------------------------------------------------------------
 
 def cpu_baseline(cfg, dm, y, budget_s=12.0):
-    import torch
+    """numpy oracle (bit-identical restatement of the reference), 1 core."""
     from threadpoolctl import threadpool_limits
     from oracle import bak_oracle as orc
-    cores = 1
     if cfg["kind"] == "batched":
-        data, obs = dm.data, dm.obs
-        n = 0
-        t0 = time.perf_counter()
-        while time.perf_counter() - t0 < budget_s and n < dm.nsys:
-            x = np.asfortranarray(data[n, :, :obs].cpu().numpy().T)
+        n, busy = 0, 0.0
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < budget_s and n < dm.nsys:
+            x = np.asfortranarray(dm.data[n, :, :dm.obs].cpu().numpy().T)
             yy = y[n].cpu().numpy()
             ts = time.perf_counter()
             orc.solve(x, yy, max_iter=cfg["sweeps"], tol=cfg["tol"])
-            if n == 0:
-                t0 = ts  # exclude first-call warm-up
-                n_done_t = 0.0
-            n_done_t += time.perf_counter() - ts
+            if n > 0:
+                busy += time.perf_counter() - ts
             n += 1
-        per_sys = n_done_t / n
-        sps = cfg["sweeps"] / per_sys / dm.nsys  # batch-sweeps/s
-        return {"value": sps, "unit": "sweeps/s", "cores": cores, "kind": "port",
-                "sample": f"{n} of {dm.nsys} systems solved ({cfg['sweeps']} sweeps each) by the numpy oracle "
-                          f"on 1 core; batch-sweeps/s = sweeps / (per-system time x {dm.nsys})"}
+        per_sys = busy / max(1, n - 1)
+        return {"value": cfg["sweeps"] / per_sys / dm.nsys, "unit": "sweeps/s", "cores": 1, "kind": "port",
+                "sample": f"{n - 1} of {dm.nsys} systems solved ({cfg['sweeps']} sweeps each) by the numpy oracle "
+                          f"(bit-identical restatement of baksolve.solve_bak) on 1 core; batch-sweeps/s = "
+                          f"sweeps / (per-system time x {dm.nsys})"}
     obs, nv = dm.obs, dm.vars
-    # a full-length column sample: per-column cost at the real obs
     ncs = min(nv, 32 if obs >= (1 << 22) else (256 if obs >= 100_000 else nv))
     if cfg["kind"] == "c4":
         ncs = 20_000
@@ -213,179 +219,260 @@ def cpu_baseline(cfg, dm, y, budget_s=12.0):
             if time.perf_counter() - t0 > budget_s * 0.5:
                 break
         t = time.perf_counter() - t0
-    t_col = t / cols_done
-    sps = 1.0 / (t_col * nv)
-    return {"value": sps, "unit": "sweeps/s", "cores": cores, "kind": "port",
+    return {"value": 1.0 / (t / cols_done * nv), "unit": "sweeps/s", "cores": 1, "kind": "port",
             "sample": f"{cols_done} column steps of the numpy oracle (bit-identical restatement of "
-                      f"baksolve.bak._run_sweeps) on the first {ncs} full-length columns ({obs} rows), "
-                      f"1 core; sweeps/s = 1/(t_col x {nv} columns)"}
+                      f"baksolve.bak._run_sweeps) on the first {ncs} full-length columns ({obs} rows), 1 core; "
+                      f"sweeps/s = 1/(t_col x {nv} columns)"}
+
+
+def cpu_reference_threads(cfg, dm, y, budget_s=20.0):
+    """The reference algorithm with all host threads: C/OpenMP port of oracle/."""
+    from oracle import bak_oracle_c as oc
+    nt = oc.threads()
+    if cfg["kind"] == "batched":
+        n = min(dm.nsys, max(nt * 8, 256))
+        xs = dm.data[:n].cpu().numpy()
+        ys = y[:n].cpu().numpy()
+        oc.solve_batched(xs[:nt], ys[:nt], 2, nthreads=nt)  # warm-up
+        t0 = time.perf_counter()
+        oc.solve_batched(xs, ys, cfg["sweeps"], nthreads=nt)
+        t = time.perf_counter() - t0
+        return {"value": cfg["sweeps"] * n / t / dm.nsys, "unit": "sweeps/s", "cores": nt, "kind": "port",
+                "sample": f"{n} of {dm.nsys} systems x {cfg['sweeps']} sweeps, C/OpenMP port, {nt} threads "
+                          f"(one system per thread); batch-sweeps/s scaled to {dm.nsys} systems"}
+    obs, nv = dm.obs, dm.vars
+    ncs = min(nv, 64 if obs >= (1 << 22) else (256 if obs >= 100_000 else nv))
+    if cfg["kind"] == "c4":
+        ncs = 50_000
+    x = np.asfortranarray(dm.data[:ncs, :obs].cpu().numpy().T)
+    yy = y.cpu().numpy()
+    oc.solve(x, yy, 1, nthreads=nt)  # warm-up
+    sweeps, t = 0, 0.0
+    while t < budget_s * 0.5:
+        t0 = time.perf_counter()
+        oc.solve(x, yy, 1, nthreads=nt)
+        t += time.perf_counter() - t0
+        sweeps += 1
+    t_col = t / (sweeps * ncs)
+    return {"value": 1.0 / (t_col * nv), "unit": "sweeps/s", "cores": nt, "kind": "port",
+            "sample": f"{sweeps} sweeps over the first {ncs} full-length columns ({obs} rows), C/OpenMP port "
+                      f"(rows split over {nt} threads, per-column dots summed in thread order); "
+                      f"sweeps/s = 1/(t_col x {nv} columns)"}
 
 
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
 
+def _max_over_ranks(ms, world, dev):
+    if world == 1:
+        return ms
+    import torch
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _timed(fn, steps, dev, world):
+    import torch
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    out = None
+    e0.record(st)
+    for _ in range(steps):
+        out = fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    return _max_over_ranks(e0.elapsed_time(e1), world, dev), out
+
+
 def run_ours(args, cfg, rank, world, dev):
     import torch
     import paper_2104_12570_b200 as pb
     from paper_2104_12570_b200 import _lib
     from paper_2104_12570_b200.bak import _Workspace, _ptr, _stream_ptr, _workspace_bytes
+    from paper_2104_12570_b200.sharded import DistComm, partition_rows, solve_bak_rowsharded
 
     lib = _lib.load()
     torch.cuda.set_device(dev)
-    dm, y = make_inputs(cfg, dev, seed=1234 + rank)
-    scfg = pb.SolveConfig(max_iter=cfg["sweeps"], tol=cfg["tol"])
     batched = cfg["kind"] == "batched"
+    variant = args.variant or cfg.get("variant", "auto")
     ts = 8 if cfg["dtype"] == "f64" else 4
+    sharded_rows = (not batched) and world > 1
+    if batched:
+        per = -(-cfg["nsys"] // world)
+        s0, s1 = min(cfg["nsys"], rank * per), min(cfg["nsys"], (rank + 1) * per)
+        dm, y = make_inputs(cfg, dev, seed=1234 + rank, nsys=s1 - s0)
+        local_units = dm.nsys
+    elif sharded_rows:
+        r0, r1 = partition_rows(cfg["obs"], world, rank, align=4)
+        dm, y = make_inputs(cfg, dev, seed=1234 + rank, rows=r1 - r0)
+        local_units = dm.obs
+    else:
+        dm, y = make_inputs(cfg, dev, seed=1234)
+        local_units = dm.obs
+    scfg = pb.SolveConfig(max_iter=cfg["sweeps"], tol=cfg["tol"])
+    comm = DistComm() if world > 1 else None
 
-    def step():
+    def step(v=variant):
         if batched:
             return pb.solve_bak_batched(dm, y, scfg, return_device=True)
-        return pb.solve_bak(dm, y, scfg, variant=args.variant, return_device=True)
+        if sharded_rows:
+            return solve_bak_rowsharded([dm], [y], scfg, comm, return_device=True)[0]
+        return pb.solve_bak(dm, y, scfg, variant=v, return_device=True)
 
     for _ in range(args.warmup):
         rep = step()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    sweeps_done = int(np.sum(rep.sweeps_run)) if batched else rep.sweeps_run
-    variant = "batched" if batched else rep.variant
+    used = "batched" if batched else rep.variant
 
-    # ---- value: whole solves, inputs resident in HBM ----
-    st = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ---- value: whole solves, inputs resident in HBM (max over ranks) ----
     l0 = lib.bak_launch_count()
-    total_sweeps = 0
     with ClockSampler(torch.cuda.current_device()) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        ev0.record(st)
-        for _ in range(args.steps):
-            rep = step()
-            total_sweeps += (int(rep.sweeps_run.max()) if batched else rep.sweeps_run)
-        ev1.record(st)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
+        ms, rep = _timed(step, args.steps, dev, world)
     launches = lib.bak_launch_count() - l0
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
-    units = cfg["sweeps"] * world  # sweeps of one system / one batch per rank per step
-    value = units * args.steps / (ms / 1e3)
+    sweeps_per_step = int(rep.sweeps_run.max()) if batched else rep.sweeps_run
+    value = sweeps_per_step * args.steps / (ms / 1e3)
 
-    # ---- roofline: the sweep kernel alone ----
+    # exact per-column kernel on the same inputs (labelled GRAM default -> show both)
+    exact = None
+    if cfg.get("exact") and variant == "gram" and world == 1 and not args.no_exact:
+        step(cfg["exact"])
+        ems, erep = _timed(lambda: step(cfg["exact"]), 1, dev, world)
+        exact = {"variant": erep.variant, "value": round(erep.sweeps_run / (ems / 1e3), 3),
+                 "ms_per_step": round(ems, 3), "note": "exact per-column kernel (reference rounding structure)"}
+
+    # ---- roofline: the dominant kernel alone ----
     code = dm.code
+    extra = {}
     if batched:
-        xbytes_per_sweep = dm.nsys * cfg["obs"] * cfg["vars"] * ts
-        kev0, kev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        kev0.record(st)
-        for _ in range(args.steps):
-            r = pb.solve_bak_batched(dm, y, scfg, return_device=True)
-        kev1.record(st)
-        torch.cuda.synchronize()
-        k_ms = kev0.elapsed_time(kev1) / args.steps
+        xbytes = dm.nsys * dm.obs * dm.vars * ts
+        k_ms, r = _timed(lambda: pb.solve_bak_batched(dm, y, scfg, return_device=True), args.steps, dev, 1)
+        k_ms /= args.steps
         k_sweeps = int(r.sweeps_run.max())
-        kernel = "batched_kernel (whole per-system solve, one CTA per system)"
+        kernel = "batched_kernel (whole per-system solve, one CTA per system; x resident in smem)"
+        alg_bytes = xbytes * k_sweeps
+    elif used.startswith("gram"):
+        xbytes = dm.obs * dm.vars * ts
+        nblk = lib.bak_gram_pass_blocks(dm.vars)
+        gpart = torch.zeros((nblk, dm.vars), dtype=torch.float64, device=dev)
+        sqpart = torch.zeros(nblk, dtype=torch.float64, device=dev)
+        delta = torch.full((dm.vars,), 1e-3, dtype=torch.float64, device=dev)
+        ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
+        e = y.clone()
+        st = _stream_ptr(torch, dev)
+
+        def one_pass():
+            _lib.check(lib.bak_gram_pass(code, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(e), _ptr(delta), 1, 1,
+                                         _ptr(gpart), _ptr(sqpart), _ptr(ctrl), st), "bak_gram_pass")
+        one_pass()
+        k_ms, _ = _timed(one_pass, max(3, args.steps), dev, 1)
+        k_ms /= max(3, args.steps)
+        k_sweeps = 1
+        alg_bytes = xbytes
+        kernel = "gram_pass_tma_kernel (one pass over x per sweep: e -= X d, sum e^2, g = X^T e)"
+        G = torch.empty((dm.vars, dm.vars), dtype=torch.float64, device=dev)
+        gws = _Workspace(torch, dev, lib.bak_gram_matrix_workspace(code, dm.obs, dm.vars))
+
+        def gram():
+            _lib.check(lib.bak_gram_matrix(code, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(G), gws.ptr, gws.nbytes, st),
+                       "bak_gram_matrix")
+        gram()
+        g_ms, _ = _timed(gram, 2, dev, 1)
+        g_ms /= 2
+        nb = -(-dm.vars // 64)
+        flops = 2.0 * dm.obs * (nb * (nb + 1) // 2) * 64 * 64
+        extra["gram_matrix"] = {"kernel": "gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
+                                "ms": round(g_ms, 3), "tflops": round(flops / (g_ms / 1e3) / 1e12, 2),
+                                "share_of_step": round(g_ms / (ms / args.steps), 3)}
     else:
-        ws = _Workspace(torch, dev, _workspace_bytes(lib, code, dm.obs, dm.vars, _lib.VARIANTS[args.variant]))
+        ws = _Workspace(torch, dev, _workspace_bytes(lib, code, dm.obs, dm.vars, _lib.VARIANTS.get(variant, 0)))
         norms = pb.colnorms(dm, ws)
         e = torch.empty_like(y)
         a = torch.zeros(dm.vars, dtype=y.dtype, device=dev)
         status = torch.zeros(4, dtype=torch.int64, device=dev)
-        vcode = _lib.VARIANTS[args.variant]
         k_tot = 0.0
         for _ in range(args.steps):
             e.copy_(y)
             a.zero_()
-            kev0, kev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            kev0.record(st)
-            _lib.check(lib.bak_sweep(code, vcode, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(norms), None, dm.vars, 0,
-                                     _ptr(e), _ptr(a), cfg["sweeps"], -1.0 if cfg["tol"] == 0 else
-                                     cfg["tol"] ** 2 * float((y.double() ** 2).sum()), None, _ptr(status),
-                                     ws.ptr, ws.nbytes, _stream_ptr(torch, dev)), "bak_sweep")
-            kev1.record(st)
-            torch.cuda.synchronize()
-            k_tot += kev0.elapsed_time(kev1)
+            kt, _ = _timed(lambda: _lib.check(lib.bak_sweep(
+                code, _lib.VARIANTS.get(variant, 0), dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(norms), None, dm.vars, 0,
+                _ptr(e), _ptr(a), cfg["sweeps"], -1.0, None, _ptr(status), ws.ptr, ws.nbytes,
+                _stream_ptr(torch, dev)), "bak_sweep"), 1, dev, 1)
+            k_tot += kt
         k_ms = k_tot / args.steps
         k_sweeps = int(status[0].item())
-        xbytes_per_sweep = dm.obs * dm.vars * ts
-        kernel = f"sweep_kernel[{variant}]"
-    alg_bytes = xbytes_per_sweep * k_sweeps
+        xbytes = dm.obs * dm.vars * ts
+        alg_bytes = xbytes * k_sweeps
+        kernel = f"sweep_kernel[{used}]"
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            tr = json.load(f)
-        key = f"{args.config}:{variant}"
-        if key in tr:
-            traffic = tr[key]
+            traffic = json.load(f).get(f"{args.config}:{used}")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "frac_of_spec_8000": round(achieved / SPEC_HBM_GBS, 4),
-                "peak_source": peak_kind, "traffic": traffic, "kernel": kernel,
-                "kernel_ms": round(k_ms, 4), "alg_bytes_per_launch": alg_bytes,
-                "sweeps_per_launch": k_sweeps}
+                "peak_source": peak_kind, "traffic": traffic, "kernel": kernel, "kernel_ms": round(k_ms, 4),
+                "alg_bytes_per_launch": int(alg_bytes), "sweeps_per_launch": k_sweeps, **extra}
 
-    # ---- e2e: through solve_bak with pinned host buffers ----
+    # ---- e2e: through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        if batched:
+        try:
             hx = torch.empty(dm.data.shape, dtype=dm.data.dtype, pin_memory=True)
-            hx.copy_(dm.data)
-            hxv = hx.transpose(1, 2)[:, :cfg["obs"], :]  # (nsys, obs, vars) view
-            hy = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
-            hy.copy_(y)
-            h2d = hx.numel() * ts + hy.numel() * ts
+            pinned = True
+        except RuntimeError:  # host cannot pin that much: pageable host memory
+            hx = torch.empty(dm.data.shape, dtype=dm.data.dtype)
+            pinned = False
+        hx.copy_(dm.data)
+        hy = torch.empty(y.shape, dtype=y.dtype, pin_memory=pinned)
+        hy.copy_(y)
+        h2d = hx.numel() * ts + hy.numel() * ts
+        if batched:
+            hxv = hx.transpose(1, 2)[:, : dm.obs, :]
 
             def e2e_step():
                 r = pb.solve_bak_batched(hxv, hy, scfg)
                 return r, r.a_hat.nbytes + r.residual.nbytes + r.sweeps_run.nbytes * 4
         else:
-            hx = torch.empty(dm.data.shape, dtype=dm.data.dtype, pin_memory=True)
-            hx.copy_(dm.data)
-            hxv = hx.t()[: dm.obs]  # (obs, vars) column-major view of the pinned buffer
-            hy = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
-            hy.copy_(y)
-            h2d = hx.numel() * ts + hy.numel() * ts
+            hxv = hx.t()[: dm.obs]
 
             def e2e_step():
-                r = pb.solve_bak(hxv, hy, scfg, variant=args.variant)
+                if sharded_rows:
+                    r = solve_bak_rowsharded([hxv], [hy], scfg, comm)[0]
+                else:
+                    r = pb.solve_bak(hxv, hy, scfg, variant=variant)
                 return r, r.a_hat.nbytes + r.residual.nbytes + dm.vars * ts + 64
-        r, d2h = e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        ev0.record(st)
-        for _ in range(args.steps):
-            r, d2h = e2e_step()
-        ev1.record(st)
-        torch.cuda.synchronize()
-        ems = ev0.elapsed_time(ev1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": units * args.steps / (ems / 1e3), "unit": "sweeps/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems / args.steps, 3)}
+        e2e_step()
+        ems, (r, d2h) = _timed(e2e_step, args.steps, dev, world)
+        e2e = {"value": round(sweeps_per_step * args.steps / (ems / 1e3), 3), "unit": "sweeps/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(ems / args.steps, 3), "per_rank_shard": world > 1, "pinned": pinned}
         del hx, hy
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (seeded device RNG, reference distributions and shapes)",
         "config": {"workload": args.config, "desc": cfg["desc"], "obs": cfg["obs"], "vars": cfg["vars"],
                    "nsys": cfg.get("nsys", 1), "sweeps_per_step": cfg["sweeps"], "tol": cfg["tol"],
-                   "variant": variant, "x_gb_per_sweep": round(xbytes_per_sweep / 1e9, 4),
-                   "x_stream_gbs_whole_solve": round(xbytes_per_sweep * total_sweeps / (ms / 1e3) / 1e9, 1),
-                   "l2": "inputs larger than L2 (126 MB)" if xbytes_per_sweep > 126e6 else
-                         "x fits in L2: re-read each sweep from L2 by design",
-                   "parallelism": f"dp{world}" if world > 1 else "single"},
+                   "variant": used + (" (labelled algebraically-equivalent sweep)" if used.startswith("gram") else ""),
+                   "exact_variant": exact,
+                   "rows_or_systems_per_rank": int(local_units),
+                   "x_gb_per_sweep_total": round(cfg.get("nsys", 1) * cfg["obs"] * cfg["vars"] * ts / 1e9, 4),
+                   "x_stream_gbs_whole_solve": round(cfg.get("nsys", 1) * cfg["obs"] * cfg["vars"] * ts
+                                                     * sweeps_per_step * args.steps / (ms / 1e3) / 1e9, 1),
+                   "l2": "inputs larger than L2 (126 MB)" if cfg.get("nsys", 1) * cfg["obs"] * cfg["vars"] * ts
+                         > 126e6 else "x fits in L2",
+                   "parallelism": (f"row-shard x{world}" if sharded_rows else
+                                   (f"system-shard x{world}" if world > 1 else "single"))},
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -397,25 +484,22 @@ def run_ours(args, cfg, rank, world, dev):
 
 
 def run_reference(args, cfg, rank, world):
-    """The reference arm: the CPU port of the reference algorithm on this host."""
+    """Reference arm: the reference algorithm on this host's CPU (rank 0 only)."""
     if rank != 0:
         return None
     import torch
-    dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
-    if dev is not None:
-        dm, y = make_inputs(cfg, dev, seed=1234)
-    else:  # CPU-only host: same shapes from the oracle generator (small configs only)
-        raise SystemExit(json.dumps({"impl": "reference", "unavailable": "needs the synthetic inputs; no device"}))
-    vals = []
-    cb = None
+    if not torch.cuda.is_available():
+        return {"impl": "reference", "unavailable": "synthetic inputs are generated on the GPU; no device"}
+    dm, y = make_inputs(cfg, torch.device("cuda", 0), seed=1234)
+    vals, cb = [], None
     for _ in range(max(1, args.steps)):
-        cb = cpu_baseline(cfg, dm, y, budget_s=max(4.0, 60.0 / max(1, args.steps)))
+        cb = cpu_reference_threads(cfg, dm, y, budget_s=max(4.0, 60.0 / max(1, args.steps)))
         vals.append(cb["value"])
     v = float(np.median(vals))
     cb["value"] = v
     return {"metric": METRIC, "value": v, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": cfg["dtype"], "data": "synthetic",
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic (seeded, reference distributions and shapes)",
             "config": {"workload": args.config, "desc": cfg["desc"], "obs": cfg["obs"], "vars": cfg["vars"],
                        "nsys": cfg.get("nsys", 1), "sweeps_per_step": cfg["sweeps"]},
             "impl": "reference", "cpu_baseline": cb,
@@ -428,10 +512,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
-    ap.add_argument("--variant", default="auto")
+    ap.add_argument("--variant", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-exact", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -98,6 +98,30 @@ int bak_sweep(int dtype, int variant,
 /* Variant AUTO would pick for this shape (for reporting). */
 int bak_sweep_pick_variant(int dtype, int64_t obs, int64_t vars);
 
+/* ---- GRAM building blocks (BAK_VARIANT_GRAM, exposed for row sharding) -------
+ * The labelled, algebraically equivalent sweep: one pass over x per sweep
+ * (e -= X d; sum e^2; g = X^T e) plus a forward substitution with G = X^T X.
+ * bak_gram_matrix : G (vars x vars, fp64, full symmetric) of the given rows.
+ * bak_gram_pass   : writes bak_gram_pass_blocks(vars) partial rows of g
+ *                   (gpart[b*vars + j]) and of sum e^2 (sqpart[b]); no-op when
+ *                   *done_flag != 0.  apply=0: no update; dot=0: no g.
+ * bak_gram_solve  : sums nparts partials in index order, finalizes sweep-1
+ *                   (history, early break -> ctrl[0]=done, ctrl[1]=sweeps,
+ *                   ctrl[2]=converged; status as bak_sweep) and, unless done,
+ *                   computes d for `sweep` (a += d, delta = d). ctrl: int64[4],
+ *                   zeroed by the caller before the first solve. */
+int bak_gram_pass_blocks(int64_t vars);
+int64_t bak_gram_matrix_workspace(int dtype, int64_t obs, int64_t vars);
+int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
+                  const double* delta, int apply, int dot, double* gpart, double* sqpart,
+                  const int64_t* done_flag, void* stream);
+int bak_gram_solve(int dtype, int64_t vars, const double* gpart, const double* sqpart, int64_t nparts,
+                   int64_t sweep, int64_t max_iter, double thresh2, const int32_t* cols, int64_t ncols,
+                   int64_t cols_stride, const void* norms2, const double* G, void* a, double* delta,
+                   double* history, int64_t* ctrl, int64_t* status, void* stream);
+
 /* ---- (4) batched many-small-systems solve ---------------------------------
  * One CTA per system; each CTA runs the whole solve_bak (bak.py:146-195) for
  * its system: e = y (or y - x a0), sweeps, early break, final residual and drift.

@@ -332,3 +332,77 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
 }
 
 }  // namespace bak
+
+// ======================= C ABI: GRAM building blocks =========================
+// Used directly for row-sharded multi-GPU solves (each rank: local G and pass
+// partials; the host gathers the partials of all ranks, rank-major, and every
+// rank runs the same solve on the same bytes -> bit-identical d and a).
+using namespace bak;
+
+extern "C" int bak_gram_pass_blocks(int64_t vars) {
+  return gram_tma_supported(vars) ? gram_tma_grid() : static_cast<int>(gram_nblk());
+}
+
+extern "C" int64_t bak_gram_matrix_workspace(int dtype, int64_t obs, int64_t vars) {
+  (void)dtype;
+  int nchunks;
+  int64_t chunk;
+  return gram_g_workspace(obs, vars, nchunks, chunk) + 256;
+}
+
+extern "C" int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
+                               void* workspace, int64_t workspace_bytes, void* stream) {
+  if ((dtype != BAK_F32 && dtype != BAK_F64) || obs < 1 || vars < 1 || ldx < obs || !x || !G) {
+    set_error("bak_gram_matrix: bad arguments");
+    return BAK_EINVAL;
+  }
+  const size_t ts = dtype_size(dtype);
+  if (reinterpret_cast<uintptr_t>(x) % 16 || (ldx * static_cast<int64_t>(ts)) % 16) {
+    set_error("bak_gram_matrix: x must be 16-byte aligned with ldx*sizeof(T) %% 16 == 0");
+    return BAK_EINVAL;
+  }
+  return launch_gram_g(dtype, x, obs, ldx, vars, G, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
+                             const double* delta, int apply, int dot, double* gpart, double* sqpart,
+                             const int64_t* done_flag, void* stream) {
+  if ((dtype != BAK_F32 && dtype != BAK_F64) || obs < 1 || !gram_supported(vars) || ldx < obs || !x || !e ||
+      !delta || !gpart || !sqpart || !done_flag) {
+    set_error("bak_gram_pass: bad arguments");
+    return BAK_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (gram_tma_supported(vars))
+    return launch_gram_pass_tma(dtype, x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart, done_flag, st);
+  PassParams pp{x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart,
+                reinterpret_cast<const GramCtrl*>(done_flag)};
+  if (dtype == BAK_F64)
+    gram_pass_kernel<double><<<static_cast<unsigned>(gram_nblk()), kGT, 0, st>>>(pp);
+  else
+    gram_pass_kernel<float><<<static_cast<unsigned>(gram_nblk()), kGT, 0, st>>>(pp);
+  count_launches(1);
+  BAK_CHECK_CUDA(cudaGetLastError());
+  return BAK_OK;
+}
+
+extern "C" int bak_gram_solve(int dtype, int64_t vars, const double* gpart, const double* sqpart, int64_t nparts,
+                              int64_t sweep, int64_t max_iter, double thresh2, const int32_t* cols, int64_t ncols,
+                              int64_t cols_stride, const void* norms2, const double* G, void* a, double* delta,
+                              double* history, int64_t* ctrl, int64_t* status, void* stream) {
+  if ((dtype != BAK_F32 && dtype != BAK_F64) || !gram_supported(vars) || !gpart || !sqpart || nparts < 1 ||
+      sweep < 1 || !norms2 || !G || !a || !delta || !ctrl || (!cols && ncols != vars)) {
+    set_error("bak_gram_solve: bad arguments");
+    return BAK_EINVAL;
+  }
+  SolveParams sp{vars, nparts, sweep, max_iter, thresh2, cols, ncols, cols_stride, norms2, G, gpart, sqpart,
+                 a, delta, history, reinterpret_cast<GramCtrl*>(ctrl), status};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == BAK_F64)
+    gram_solve_kernel<double><<<1, 512, 0, st>>>(sp);
+  else
+    gram_solve_kernel<float><<<1, 512, 0, st>>>(sp);
+  count_launches(1);
+  BAK_CHECK_CUDA(cudaGetLastError());
+  return BAK_OK;
+}

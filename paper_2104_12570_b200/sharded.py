@@ -1,0 +1,226 @@
+"""(5) Multi-GPU row sharding of one very tall system (BASELINE config 3 at N > 1).
+
+One process per GPU; rank r holds a contiguous block of rows of x, y and e
+(``partition_rows``); the coefficients a and the column norms are replicated.
+The per-sweep exchange is the GRAM variant's: every rank makes ONE pass over
+its rows (e -= X d, sum e^2, partial g = X^T e), the ranks all-gather their
+partials (a few hundred KB), and every rank runs the same forward substitution
+on the same bytes summed in rank order - so d and a are bit-identical on all
+ranks without a broadcast.  G = X^T X is all-gathered once.  The sweep is the
+labelled GRAM reformulation (bak_gram.cu): same iterates as the reference in
+exact arithmetic; parity is checked like every other variant.
+
+``Comm`` abstracts the only collective used (all-gather, rank order):
+``DistComm`` wraps torch.distributed (NCCL between GPUs, gloo on CPU) and
+``LocalComm`` emulates N ranks inside one process (the shards live on one
+device and the kernels of different ranks never wait on one another), which
+is how the multi-rank path is tested on a single GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _lib
+from .bak import (DRIFT_TOL, DeviceMatrix, SolveConfig, SolveReport, _permutation_chunks, _ptr, _stream_ptr,
+                  _to_device_vector, _torch, _Workspace, colnorms, to_device_matrix)
+
+
+def partition_rows(obs, world, rank, align=2):
+    """Contiguous row block [r0, r1) of `rank`; block starts are multiples of
+    `align` rows (16-byte aligned columns for both precisions when align=4)."""
+    per = -(-obs // world)
+    per = -(-per // align) * align
+    r0 = min(obs, rank * per)
+    r1 = min(obs, r0 + per)
+    return r0, r1
+
+
+def rank_order_sum(tensors):
+    """Elementwise sum in rank order (fixed, identical on every rank)."""
+    out = tensors[0].clone()
+    for t in tensors[1:]:
+        out += t
+    return out
+
+
+class LocalComm:
+    """N emulated ranks in one process: all_gather of the per-rank list is the list itself."""
+
+    def __init__(self, world):
+        self.world = world
+
+    def all_gather(self, per_rank):
+        assert len(per_rank) == self.world
+        return list(per_rank)
+
+
+class DistComm:
+    """One rank per process over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, per_rank):
+        assert len(per_rank) == 1
+        t = per_rank[0].contiguous()
+        out = t.new_empty((self.world * t.numel(),))
+        self.dist.all_gather_into_tensor(out, t.reshape(-1), group=self.group)
+        return [out[r * t.numel():(r + 1) * t.numel()].view(t.shape) for r in range(self.world)]
+
+
+class _Shard:
+    def __init__(self, dm, y, ws):
+        self.dm = dm
+        self.y = y
+        self.ws = ws
+
+
+def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, comm=None, a0=None, *,
+                         return_device=False):
+    """Solve one system whose rows are split over ranks.
+
+    x_shards / y_shards: list of this process's shards (one for DistComm; all N
+    for LocalComm), each a (rows_r, vars) matrix (numpy / torch / DeviceMatrix)
+    and its (rows_r,) target.  Returns one SolveReport per local shard: a_hat is
+    the (replicated) coefficient vector, residual the shard's rows of y - x a.
+    """
+    cfg = config if config is not None else SolveConfig()
+    torch = _torch()
+    lib = _lib.load()
+    if comm is None:
+        comm = LocalComm(len(x_shards))
+    shards = []
+    for xs, ys in zip(x_shards, y_shards):
+        dm = to_device_matrix(xs)
+        yd = _to_device_vector(ys, dm.np_dtype, dm.data.device)
+        if yd.shape[0] != dm.obs:
+            raise ValueError(f"y has length {yd.shape[0]}, expected {dm.obs}")
+        shards.append(_Shard(dm, yd, None))
+    nv = shards[0].dm.vars
+    code = shards[0].dm.code
+    if any(s.dm.vars != nv or s.dm.code != code for s in shards):
+        raise ValueError("shards must share vars and dtype")
+    dev = shards[0].dm.data.device
+    st = _stream_ptr(torch, dev)
+    t0 = time.perf_counter()
+    for s in shards:
+        wsb = max(lib.bak_gram_matrix_workspace(code, s.dm.obs, nv), lib.bak_colnorms_workspace(code, s.dm.obs, nv),
+                  lib.bak_residual_workspace(code, s.dm.obs, nv), 1 << 16)
+        s.ws = _Workspace(torch, dev, wsb)
+
+    # ||y||^2, column norms and G: local pieces, gathered, summed in rank order
+    def local_sumsq(s):
+        out = torch.empty(1, dtype=s.y.dtype, device=dev)
+        _lib.check(lib.bak_colnorms(code, _ptr(s.y), s.dm.obs, 1, s.dm.obs, _ptr(out), s.ws.ptr, s.ws.nbytes, st),
+                   "bak_colnorms(y)")
+        return out.double()
+
+    ynorm2 = float(rank_order_sum(comm.all_gather([local_sumsq(s) for s in shards])).item())
+    tdt = shards[0].y.dtype
+    if ynorm2 == 0.0:
+        reps = []
+        for s in shards:
+            a_z = torch.zeros(nv, dtype=tdt, device=dev)
+            r_z = torch.zeros(s.dm.obs, dtype=tdt, device=dev)
+            reps.append(SolveReport(a_z if return_device else a_z.cpu().numpy(),
+                                    r_z if return_device else r_z.cpu().numpy(),
+                                    [] if cfg.record_history else None, 0, True, time.perf_counter() - t0,
+                                    variant="gram-rowshard"))
+        return reps
+    norms = rank_order_sum(comm.all_gather([colnorms(s.dm, s.ws).double() for s in shards])).to(tdt)
+    norms_h = norms.cpu().numpy()
+    if not norms_h.any():
+        raise ValueError("every column of x has zero norm; nothing to solve")
+    G_parts = []
+    for s in shards:
+        G = torch.empty((nv, nv), dtype=torch.float64, device=dev)
+        _lib.check(lib.bak_gram_matrix(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(G), s.ws.ptr, s.ws.nbytes, st),
+                   "bak_gram_matrix")
+        G_parts.append(G)
+    G = rank_order_sum(comm.all_gather(G_parts))
+
+    if a0 is not None:
+        a = _to_device_vector(a0, shards[0].dm.np_dtype, dev, "a0").clone()
+        if a.shape[0] != nv:
+            raise ValueError(f"a0 has length {a.shape[0]}, expected {nv}")
+    else:
+        a = torch.zeros(nv, dtype=tdt, device=dev)
+    for s in shards:
+        s.e = torch.empty_like(s.y)
+        if a0 is not None:
+            _lib.check(lib.bak_residual(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(a), _ptr(s.y), _ptr(s.e),
+                                        s.ws.ptr, s.ws.nbytes, st), "bak_residual")
+        else:
+            s.e.copy_(s.y)
+    thresh2 = cfg.tol * cfg.tol * ynorm2 if cfg.tol > 0 else -1.0
+    nblk = lib.bak_gram_pass_blocks(nv)
+    for s in shards:
+        s.gpart = torch.zeros((nblk, nv), dtype=torch.float64, device=dev)
+        s.sqpart = torch.zeros(nblk, dtype=torch.float64, device=dev)
+    delta = torch.zeros(nv, dtype=torch.float64, device=dev)
+    ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    hist = torch.zeros(cfg.max_iter, dtype=torch.float64, device=dev) if cfg.record_history else None
+    nz_mask = norms_h != 0
+    if cfg.ordering == "cyclic":
+        if nz_mask.all():
+            cols_all, ncols, stride = None, nv, 0
+        else:
+            cols_all = torch.from_numpy(np.flatnonzero(nz_mask).astype(np.int32)).to(dev)
+            ncols, stride = int(cols_all.numel()), 0
+    else:
+        gen = _permutation_chunks(cfg.ordering_seed, nv, None if nz_mask.all() else nz_mask)
+        perms = np.stack([next(gen) for _ in range(cfg.max_iter)]).astype(np.int32)
+        cols_all = torch.from_numpy(perms).to(dev)
+        ncols, stride = perms.shape[1], perms.shape[1]
+
+    def passes(apply, dot):
+        for s in shards:
+            _lib.check(lib.bak_gram_pass(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(s.e), _ptr(delta), apply, dot,
+                                         _ptr(s.gpart), _ptr(s.sqpart), _ptr(ctrl), st), "bak_gram_pass")
+        gp = comm.all_gather([s.gpart for s in shards])
+        sp = comm.all_gather([s.sqpart for s in shards])
+        return torch.cat([g.reshape(-1) for g in gp]), torch.cat(sp)
+
+    def solve(gp, sp, sweep):
+        _lib.check(lib.bak_gram_solve(code, nv, _ptr(gp), _ptr(sp), sp.numel(), sweep, cfg.max_iter, thresh2,
+                                      _ptr(cols_all), ncols, stride, _ptr(norms), _ptr(G), _ptr(a), _ptr(delta),
+                                      _ptr(hist), _ptr(ctrl), _ptr(status), st), "bak_gram_solve")
+
+    gp, sp = passes(0, 1)
+    for sweep in range(1, cfg.max_iter + 1):
+        solve(gp, sp, sweep)
+        gp, sp = passes(1, 1 if sweep < cfg.max_iter else 0)
+        if thresh2 >= 0 and sweep % 16 == 0 and int(ctrl[0].item()):
+            break
+    solve(gp, sp, cfg.max_iter + 1)
+    stat = status.cpu().numpy()
+    sweeps, converged = int(stat[0]), bool(stat[1])
+
+    resids = []
+    d2_parts = []
+    for s in shards:
+        r = torch.empty_like(s.y)
+        _lib.check(lib.bak_residual(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(a), _ptr(s.y), _ptr(r), s.ws.ptr,
+                                    s.ws.nbytes, st), "bak_residual")
+        d2 = torch.empty(1, dtype=torch.float64, device=dev)
+        _lib.check(lib.bak_diff_norm2(code, _ptr(s.e), _ptr(r), s.dm.obs, _ptr(d2), s.ws.ptr, s.ws.nbytes, st),
+                   "bak_diff_norm2")
+        resids.append(r)
+        d2_parts.append(d2)
+    drift = float(np.sqrt(rank_order_sum(comm.all_gather(d2_parts)).item()))
+    wall = time.perf_counter() - t0
+    drift_warn = bool(drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny) > DRIFT_TOL)
+    history = hist[:sweeps].cpu().tolist() if hist is not None else None
+    a_out = a if return_device else a.cpu().numpy()
+    return [SolveReport(a_hat=a_out, residual=r if return_device else r.cpu().numpy(), residual_norm_history=history,
+                        sweeps_run=sweeps, converged=converged, wall_time=wall, drift_warning=drift_warn,
+                        variant="gram-rowshard") for r in resids]

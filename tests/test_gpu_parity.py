@@ -232,3 +232,35 @@ def test_gram_variant_random_order_zero_columns_early_break():
         assert rep.a_hat[7] == 7.5
         assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"],
                       ref_hist=ref["residual_norm_history"])
+
+
+@pytest.mark.parametrize("precision,nshards", [("double", 3), ("single", 2), ("double", 1)])
+def test_rowsharded_gram_emulated_ranks(precision, nshards):
+    """N ranks emulated in one process (LocalComm): rows split as on N GPUs,
+    partials exchanged in rank order; must match the oracle on the full system."""
+    from paper_2104_12570_b200.sharded import LocalComm, partition_rows, solve_bak_rowsharded
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=100_003, nvars=40, precision=precision)
+    blocks = [partition_rows(x.shape[0], nshards, r, align=4) for r in range(nshards)]
+    xs = [x[r0:r1] for r0, r1 in blocks]
+    ys = [y[r0:r1] for r0, r1 in blocks]
+    cfg = dict(max_iter=7, tol=0, record_history=True)
+    reps = solve_bak_rowsharded(xs, ys, pb.SolveConfig(**cfg), LocalComm(nshards))
+    ref = orc.solve(x, y, **cfg)
+    for rep in reps:
+        assert rep.a_hat.tobytes() == reps[0].a_hat.tobytes()  # replicated bit-identically
+    full = reps[0]
+    full.residual = np.concatenate([r.residual for r in reps])
+    assert_parity(x, y, full, ref["a_hat"], ref["sweeps_run"], ref["converged"], ref_hist=ref["residual_norm_history"])
+
+
+def test_rowsharded_early_break_matches_oracle():
+    from paper_2104_12570_b200.sharded import LocalComm, partition_rows, solve_bak_rowsharded
+    pb = _pb()
+    x, y, _ = orc.make_system(60_000, 30, 8, "normal", "uniform", 0.0, "double")
+    blocks = [partition_rows(x.shape[0], 4, r, align=4) for r in range(4)]
+    reps = solve_bak_rowsharded([x[a:b] for a, b in blocks], [y[a:b] for a, b in blocks],
+                                pb.SolveConfig(max_iter=200, tol=1e-11), LocalComm(4))
+    ref = orc.solve(x, y, max_iter=200, tol=1e-11)
+    assert reps[0].sweeps_run == ref["sweeps_run"] and reps[0].converged
+    assert orc.rel_coeff_err(reps[0].a_hat, ref["a_hat"]) <= 1e-10

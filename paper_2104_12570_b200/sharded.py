@@ -224,3 +224,81 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
     return [SolveReport(a_hat=a_out, residual=r if return_device else r.cpu().numpy(), residual_norm_history=history,
                         sweeps_run=sweeps, converged=converged, wall_time=wall, drift_warning=drift_warn,
                         variant="gram-rowshard") for r in resids]
+
+
+# --------------------------------------------------------------------------
+# exact per-column row sharding: in-kernel cross-GPU exchange per column
+# --------------------------------------------------------------------------
+
+class Mailboxes:
+    """Per-rank mailbox buffers for bak_sweep_rowshard plus the peer pointers.
+
+    DistComm: each rank allocates its mailbox, exports a CUDA IPC handle, the
+    handles are all-gathered and every rank maps its peers' mailboxes (NVLink
+    peer memory).  local=N: N emulated ranks share one device buffer.
+    Epochs only ever increase (``next_epochs``) so mailboxes are never reset.
+    """
+
+    def __init__(self, nranks, comm=None, device=None):
+        torch = _torch()
+        lib = _lib.load()
+        self.nranks = nranks
+        self.epoch = 0
+        per = int(lib.bak_mailbox_bytes(nranks))
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self._opened = []
+        if comm is None or isinstance(comm, LocalComm):
+            self.buf = torch.zeros(nranks * per, dtype=torch.uint8, device=dev)
+            self.ptrs = [self.buf.data_ptr() + r * per for r in range(nranks)]
+        else:
+            self.buf = torch.zeros(per, dtype=torch.uint8, device=dev)
+            torch.cuda.synchronize()
+            h = (ctypes.c_uint8 * 64)()
+            _lib.check(lib.bak_ipc_get_handle(ctypes.c_void_p(self.buf.data_ptr()), h), "bak_ipc_get_handle")
+            mine = torch.tensor(list(bytes(h)), dtype=torch.uint8, device=dev)
+            handles = comm.all_gather([mine])
+            self.ptrs = []
+            for r, hr in enumerate(handles):
+                if r == comm.rank:
+                    self.ptrs.append(self.buf.data_ptr())
+                    continue
+                raw = (ctypes.c_uint8 * 64)(*hr.cpu().tolist())
+                p = ctypes.c_void_p()
+                _lib.check(lib.bak_ipc_open_handle(raw, ctypes.byref(p)), "bak_ipc_open_handle")
+                self.ptrs.append(p.value)
+                self._opened.append(p.value)
+        self.array = (ctypes.c_void_p * nranks)(*self.ptrs)
+
+    def next_epochs(self, count):
+        base = self.epoch
+        self.epoch = (self.epoch + count + 2) & 0x7FFFFFFF
+        return base
+
+    def close(self):
+        lib = _lib.load()
+        for p in self._opened:
+            lib.bak_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+
+
+def sweep_rowshard(dm, e, a, norms, max_iter, thresh2, mailboxes, rank, nranks, nranks_local=1, history=None,
+                   status=None, stream=None):
+    """Launch the exact per-column row-sharded sweep (thin wrapper over the C ABI).
+
+    nranks_local > 1 emulates that many ranks in one launch on this device:
+    dm/e hold the rows of all of them (split evenly) and a/status/history hold
+    one replica per emulated rank.
+    """
+    torch = _torch()
+    lib = _lib.load()
+    dev = dm.data.device
+    st = stream if stream is not None else _stream_ptr(torch, dev)
+    ctas = max(1, (lib.bak_device_sm_count() or 148) // nranks_local)
+    ws = _Workspace(torch, dev, nranks_local * 2 * ctas * 32 + 4096)
+    if status is None:
+        status = torch.zeros(4 * nranks_local, dtype=torch.int64, device=dev)
+    base = mailboxes.next_epochs(max_iter * dm.vars + 1)
+    _lib.check(lib.bak_sweep_rowshard(dm.code, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(norms), _ptr(e), _ptr(a),
+                                      max_iter, thresh2, _ptr(history), _ptr(status), rank, nranks, mailboxes.array,
+                                      base, nranks_local, ws.ptr, ws.nbytes, st), "bak_sweep_rowshard")
+    return status

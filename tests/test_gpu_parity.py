@@ -264,3 +264,43 @@ def test_rowsharded_early_break_matches_oracle():
     ref = orc.solve(x, y, max_iter=200, tol=1e-11)
     assert reps[0].sweeps_run == ref["sweeps_run"] and reps[0].converged
     assert orc.rel_coeff_err(reps[0].a_hat, ref["a_hat"]) <= 1e-10
+
+
+@pytest.mark.parametrize("nranks,precision", [(2, "double"), (4, "double"), (3, "single"), (8, "double")])
+def test_rowshard_exact_kernel_emulated_ranks(nranks, precision):
+    """The exact per-column row-sharded kernel with its in-kernel per-column
+    rank exchange, N ranks emulated in ONE cooperative launch (their mailboxes
+    in local memory).  Every rank's replica of a must be bit-identical and
+    match the oracle; history and control flow too."""
+    import torch
+    from paper_2104_12570_b200.sharded import Mailboxes, sweep_rowshard
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=60_001, nvars=12, precision=precision)
+    x[:, 5] = 0.0  # zero-norm column stays frozen
+    cfg = dict(max_iter=6, tol=0, record_history=True)
+    ref = orc.solve(x, y, **cfg)
+    dm = pb.to_device_matrix(x)
+    norms = pb.colnorms(dm)
+    dev = dm.data.device
+    tdt = torch.float64 if precision == "double" else torch.float32
+    e = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
+    a = torch.zeros(nranks * 12, dtype=tdt, device=dev)
+    hist = torch.zeros(nranks * 6, dtype=torch.float64, device=dev)
+    mb = Mailboxes(nranks)
+    status = sweep_rowshard(dm, e, a, norms, 6, -1.0, mb, 0, nranks, nranks_local=nranks, history=hist)
+    st = status.cpu().numpy().reshape(nranks, 4)
+    assert np.all(st[:, 0] == 6) and np.all(st[:, 2] == 0)
+    A = a.cpu().numpy().reshape(nranks, 12)
+    for r in range(1, nranks):
+        assert A[r].tobytes() == A[0].tobytes()
+    H = hist.cpu().numpy().reshape(nranks, 6)
+    assert np.array_equal(H[0], H[-1])
+    tol = TOL[np.dtype(x.dtype)]
+    assert orc.rel_coeff_err(A[0], ref["a_hat"]) <= tol
+    assert A[0][5] == 0.0
+    np.testing.assert_allclose(H[0], ref["residual_norm_history"], rtol=max(1e3 * tol, 1e-6))
+    # a second call on the same mailboxes (epochs keep increasing, no reset)
+    a2 = torch.zeros_like(a)
+    e2 = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
+    sweep_rowshard(dm, e2, a2, norms, 6, -1.0, mb, 0, nranks, nranks_local=nranks)
+    assert a2.cpu().numpy().reshape(nranks, 12)[0].tobytes() == A[0].tobytes()

@@ -323,7 +323,8 @@ def run_ours(args, cfg, rank, world, dev):
         if batched:
             return pb.solve_bak_batched(dm, y, scfg, return_device=True)
         if sharded_rows:
-            return solve_bak_rowsharded([dm], [y], scfg, comm, return_device=True)[0]
+            return solve_bak_rowsharded([dm], [y], scfg, comm, variant="stream" if v == "stream" else "gram",
+                                        return_device=True)[0]
         return pb.solve_bak(dm, y, scfg, variant=v, return_device=True)
 
     for _ in range(args.warmup):
@@ -340,7 +341,7 @@ def run_ours(args, cfg, rank, world, dev):
 
     # exact per-column kernel on the same inputs (labelled GRAM default -> show both)
     exact = None
-    if cfg.get("exact") and variant == "gram" and world == 1 and not args.no_exact:
+    if cfg.get("exact") and variant == "gram" and not args.no_exact:
         step(cfg["exact"])
         ems, erep = _timed(lambda: step(cfg["exact"]), 1, dev, world)
         exact = {"variant": erep.variant, "value": round(erep.sweeps_run / (ems / 1e3), 3),
@@ -445,7 +446,8 @@ def run_ours(args, cfg, rank, world, dev):
 
             def e2e_step():
                 if sharded_rows:
-                    r = solve_bak_rowsharded([hxv], [hy], scfg, comm)[0]
+                    r = solve_bak_rowsharded([hxv], [hy], scfg, comm,
+                                             variant="stream" if variant == "stream" else "gram")[0]
                 else:
                     r = pb.solve_bak(hxv, hy, scfg, variant=variant)
                 return r, r.a_hat.nbytes + r.residual.nbytes + dm.vars * ts + 64

@@ -84,14 +84,22 @@ class _Shard:
 
 
 def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, comm=None, a0=None, *,
-                         return_device=False):
+                         variant="gram", return_device=False):
     """Solve one system whose rows are split over ranks.
 
     x_shards / y_shards: list of this process's shards (one for DistComm; all N
     for LocalComm), each a (rows_r, vars) matrix (numpy / torch / DeviceMatrix)
     and its (rows_r,) target.  Returns one SolveReport per local shard: a_hat is
     the (replicated) coefficient vector, residual the shard's rows of y - x a.
+
+    variant="gram"  : one pass per sweep, partials all-gathered per sweep (labelled
+                      reformulation, any ordering).
+    variant="stream": the EXACT per-column sweep; every column's partial dot is
+                      all-reduced inside the kernel through peer-mapped mailboxes
+                      (one shard per process, cyclic ordering).
     """
+    if variant not in ("gram", "stream"):
+        raise ValueError(f"unknown variant {variant!r}")
     cfg = config if config is not None else SolveConfig()
     torch = _torch()
     lib = _lib.load()
@@ -139,14 +147,6 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
     norms_h = norms.cpu().numpy()
     if not norms_h.any():
         raise ValueError("every column of x has zero norm; nothing to solve")
-    G_parts = []
-    for s in shards:
-        G = torch.empty((nv, nv), dtype=torch.float64, device=dev)
-        _lib.check(lib.bak_gram_matrix(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(G), s.ws.ptr, s.ws.nbytes, st),
-                   "bak_gram_matrix")
-        G_parts.append(G)
-    G = rank_order_sum(comm.all_gather(G_parts))
-
     if a0 is not None:
         a = _to_device_vector(a0, shards[0].dm.np_dtype, dev, "a0").clone()
         if a.shape[0] != nv:
@@ -161,6 +161,37 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
         else:
             s.e.copy_(s.y)
     thresh2 = cfg.tol * cfg.tol * ynorm2 if cfg.tol > 0 else -1.0
+    if variant == "stream":
+        if len(shards) != 1 or isinstance(comm, LocalComm) and comm.world > 1:
+            raise ValueError("variant='stream' runs one shard per process (DistComm); "
+                             "use sweep_rowshard(nranks_local=N) to emulate ranks on one device")
+        if cfg.ordering != "cyclic":
+            raise ValueError("variant='stream' supports ordering='cyclic'")
+        s0 = shards[0]
+        world = getattr(comm, "world", 1)
+        rank = getattr(comm, "rank", 0)
+        mb = getattr(comm, "_bak_mailboxes", None)
+        if mb is None or mb.nranks != world:
+            mb = Mailboxes(world, comm if world > 1 else None, dev)
+            try:
+                comm._bak_mailboxes = mb
+            except AttributeError:
+                pass
+        hist = torch.zeros(cfg.max_iter, dtype=torch.float64, device=dev) if cfg.record_history else None
+        status = sweep_rowshard(s0.dm, s0.e, a, norms, cfg.max_iter, thresh2, mb, rank, world, 1, history=hist)
+        stat = status.cpu().numpy()
+        if int(stat[2]):
+            raise _lib.BakError(f"bak_sweep_rowshard device error {int(stat[2])} (3 = exchange timeout)")
+        sweeps, converged = int(stat[0]), bool(stat[1])
+        return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "stream-rowshard")
+    G_parts = []
+    for s in shards:
+        G = torch.empty((nv, nv), dtype=torch.float64, device=dev)
+        _lib.check(lib.bak_gram_matrix(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(G), s.ws.ptr, s.ws.nbytes, st),
+                   "bak_gram_matrix")
+        G_parts.append(G)
+    G = rank_order_sum(comm.all_gather(G_parts))
+
     nblk = lib.bak_gram_pass_blocks(nv)
     for s in shards:
         s.gpart = torch.zeros((nblk, nv), dtype=torch.float64, device=dev)
@@ -205,6 +236,17 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
     stat = status.cpu().numpy()
     sweeps, converged = int(stat[0]), bool(stat[1])
 
+    return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "gram-rowshard")
+
+
+def _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, label):
+    """Residual y - x a per shard (bak.py:130) and the drift flag (bak.py:133-142)."""
+    torch = _torch()
+    lib = _lib.load()
+    dev = shards[0].dm.data.device
+    st = _stream_ptr(torch, dev)
+    code = shards[0].dm.code
+    nv = shards[0].dm.vars
     resids = []
     d2_parts = []
     for s in shards:
@@ -223,7 +265,7 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
     a_out = a if return_device else a.cpu().numpy()
     return [SolveReport(a_hat=a_out, residual=r if return_device else r.cpu().numpy(), residual_norm_history=history,
                         sweeps_run=sweeps, converged=converged, wall_time=wall, drift_warning=drift_warn,
-                        variant="gram-rowshard") for r in resids]
+                        variant=label) for r in resids]
 
 
 # --------------------------------------------------------------------------

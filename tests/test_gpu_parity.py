@@ -304,3 +304,17 @@ def test_rowshard_exact_kernel_emulated_ranks(nranks, precision):
     e2 = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
     sweep_rowshard(dm, e2, a2, norms, 6, -1.0, mb, 0, nranks, nranks_local=nranks)
     assert a2.cpu().numpy().reshape(nranks, 12)[0].tobytes() == A[0].tobytes()
+
+
+def test_rowsharded_api_stream_single_process():
+    """solve_bak_rowsharded(variant='stream') on one process: the exact in-kernel
+    exchange path with N=1 must match the oracle (the N>1 exchange is covered by
+    the emulated-ranks kernel test)."""
+    from paper_2104_12570_b200.sharded import solve_bak_rowsharded
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=40_000, nvars=10, precision="double")
+    cfg = dict(max_iter=5, tol=0, record_history=True)
+    rep = solve_bak_rowsharded([x], [y], pb.SolveConfig(**cfg), variant="stream")[0]
+    ref = orc.solve(x, y, **cfg)
+    assert rep.variant == "stream-rowshard"
+    assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"], ref_hist=ref["residual_norm_history"])

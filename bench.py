@@ -359,7 +359,7 @@ def run_ours(args, cfg, rank, world, dev):
         alg_bytes = xbytes * k_sweeps
     elif used.startswith("gram"):
         xbytes = dm.obs * dm.vars * ts
-        nblk = lib.bak_gram_pass_blocks(dm.vars)
+        nblk = lib.bak_gram_pass_blocks(code, dm.vars)
         gpart = torch.zeros((nblk, dm.vars), dtype=torch.float64, device=dev)
         sqpart = torch.zeros(nblk, dtype=torch.float64, device=dev)
         delta = torch.full((dm.vars,), 1e-3, dtype=torch.float64, device=dev)

@@ -102,7 +102,7 @@ int bak_sweep_pick_variant(int dtype, int64_t obs, int64_t vars);
  * The labelled, algebraically equivalent sweep: one pass over x per sweep
  * (e -= X d; sum e^2; g = X^T e) plus a forward substitution with G = X^T X.
  * bak_gram_matrix : G (vars x vars, fp64, full symmetric) of the given rows.
- * bak_gram_pass   : writes bak_gram_pass_blocks(vars) partial rows of g
+ * bak_gram_pass   : writes bak_gram_pass_blocks(dtype, vars) partial rows of g
  *                   (gpart[b*vars + j]) and of sum e^2 (sqpart[b]); no-op when
  *                   *done_flag != 0.  apply=0: no update; dot=0: no g.
  * bak_gram_solve  : sums nparts partials in index order, finalizes sweep-1
@@ -110,7 +110,7 @@ int bak_sweep_pick_variant(int dtype, int64_t obs, int64_t vars);
  *                   ctrl[2]=converged; status as bak_sweep) and, unless done,
  *                   computes d for `sweep` (a += d, delta = d). ctrl: int64[4],
  *                   zeroed by the caller before the first solve. */
-int bak_gram_pass_blocks(int64_t vars);
+int bak_gram_pass_blocks(int dtype, int64_t vars);
 int64_t bak_gram_matrix_workspace(int dtype, int64_t obs, int64_t vars);
 int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
                     void* workspace, int64_t workspace_bytes, void* stream);

@@ -38,7 +38,7 @@ SIGNATURES = {
     "bak_sweep_pick_variant": (_int, [_int, _i64, _i64]),
     "bak_solve_batched": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _int, _vp,
                                  _i64, _dbl, _dbl, _vp, _vp, _vp]),
-    "bak_gram_pass_blocks": (_int, [_i64]),
+    "bak_gram_pass_blocks": (_int, [_int, _i64]),
     "bak_gram_matrix_workspace": (_i64, [_int, _i64, _i64]),
     "bak_gram_matrix": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),

@@ -290,7 +290,7 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
   SolveParams sp{vars, nblk, 0, prm.max_iter, prm.thresh2, prm.cols, prm.ncols, prm.cols_stride, prm.norms2,
                  G, gpart, sqpart, prm.a, delta, prm.history, ctrl, prm.status};
   const bool use_tma = gram_tma_supported(vars);
-  if (use_tma) sp.nblk = gram_tma_grid();
+  if (use_tma) sp.nblk = gram_tma_grid(dtype);
   auto pass = [&](int apply, int dot) -> int {
     if (use_tma)
       return launch_gram_pass_tma(dtype, prm.x, prm.obs, prm.ldx, vars, prm.e, delta, apply, dot, gpart, sqpart,
@@ -339,8 +339,8 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
 // rank runs the same solve on the same bytes -> bit-identical d and a).
 using namespace bak;
 
-extern "C" int bak_gram_pass_blocks(int64_t vars) {
-  return gram_tma_supported(vars) ? gram_tma_grid() : static_cast<int>(gram_nblk());
+extern "C" int bak_gram_pass_blocks(int dtype, int64_t vars) {
+  return gram_tma_supported(vars) ? gram_tma_grid(dtype) : static_cast<int>(gram_nblk());
 }
 
 extern "C" int64_t bak_gram_matrix_workspace(int dtype, int64_t obs, int64_t vars) {

@@ -128,10 +128,12 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
         af[t] = static_cast<double>(A[(wi + t * 8 + fr) * kLd + k4 + fk]);
         bf[t] = static_cast<double>(B[(wj + t * 8 + fr) * kLd + k4 + fk]);
       }
+      if (!(diag && wj > wi)) {  // the upper quadrant of a diagonal block is never used
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+          for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      }
     }
   }
   cp_async_wait<0>();
@@ -171,8 +173,10 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nchunks,
 int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk) {
   const int nb = static_cast<int>((vars + kBT - 1) / kBT);
   const int nblk = nb * (nb + 1) / 2;
-  const int want = 4 * device_sms();
-  nchunks = (want + nblk - 1) / nblk;
+  // one wave: 2 CTAs per SM (smem-bound), every CTA one block x one K-range
+  const int slots = 2 * device_sms();
+  nchunks = slots / nblk;
+  if (nchunks < 1) nchunks = 1;
   chunk = round_up((obs + nchunks - 1) / nchunks, kKT);
   nchunks = static_cast<int>((obs + chunk - 1) / chunk);
   if (nchunks < 1) nchunks = 1;

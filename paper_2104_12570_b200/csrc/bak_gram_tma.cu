@@ -48,8 +48,12 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// fp32 tiles are half the bytes for the same instructions: two CTAs per SM
+template <typename T>
+constexpr int min_blocks() { return sizeof(T) == 4 ? 2 : 1; }
+
 template <typename T, int CW>
-__global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __grid_constant__ CUtensorMap xmap,
+__global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                                                                       const TmaPassParams p) {
   if (*reinterpret_cast<const volatile int64_t*>(p.done)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -195,7 +199,7 @@ int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStre
 
 bool gram_tma_supported(int64_t vars) { return vars >= 1 && vars <= 256 && encode_fn() != nullptr; }
 
-int gram_tma_grid() { return device_sms(); }
+int gram_tma_grid(int dtype) { return (dtype == BAK_F32 ? 2 : 1) * device_sms(); }
 
 // x: column-major obs x vars, ldx*sizeof(T) % 16 == 0
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
@@ -222,7 +226,7 @@ int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int
     return BAK_ECUDA;
   }
   TmaPassParams p{obs, vars, (obs + kR - 1) / kR, e, delta, apply, dot, gpart, sqpart, done};
-  const int grid = gram_tma_grid();
+  const int grid = gram_tma_grid(dtype);
   if (dtype == BAK_F64) {
     if (cw == 8) return launch_cw<double, 8>(map, p, grid, st);
     if (cw == 16) return launch_cw<double, 16>(map, p, grid, st);

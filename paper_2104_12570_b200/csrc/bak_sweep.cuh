@@ -58,7 +58,7 @@ int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
                   int64_t part_bytes, cudaStream_t st);
 bool gram_tma_supported(int64_t vars);
-int gram_tma_grid();
+int gram_tma_grid(int dtype);
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
                          const double* delta, int apply, int dot, double* gpart, double* sqpart, const int64_t* done,
                          cudaStream_t st);

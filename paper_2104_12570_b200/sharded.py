@@ -192,7 +192,7 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
         G_parts.append(G)
     G = rank_order_sum(comm.all_gather(G_parts))
 
-    nblk = lib.bak_gram_pass_blocks(nv)
+    nblk = lib.bak_gram_pass_blocks(code, nv)
     for s in shards:
         s.gpart = torch.zeros((nblk, nv), dtype=torch.float64, device=dev)
         s.sqpart = torch.zeros(nblk, dtype=torch.float64, device=dev)

@@ -58,8 +58,8 @@ constexpr int64_t kSlotBytes = kGridSlotBytes;  // grid / stream exchange record
 
 int pick_variant(int dtype, int64_t obs) {
   SweepPlan pl;
-  if (obs <= 2048 && plan_onchip(dtype, BAK_VARIANT_CTA, obs, pl)) return BAK_VARIANT_CTA;
-  if (obs <= 65536 && plan_onchip(dtype, BAK_VARIANT_CLUSTER, obs, pl)) return BAK_VARIANT_CLUSTER;
+  if (obs <= 1024 && plan_onchip(dtype, BAK_VARIANT_CTA, obs, pl)) return BAK_VARIANT_CTA;
+  if (obs <= 16 * 256 * 8 && plan_onchip(dtype, BAK_VARIANT_CLUSTER, obs, pl)) return BAK_VARIANT_CLUSTER;
   if (plan_onchip(dtype, BAK_VARIANT_GRID, obs, pl)) return BAK_VARIANT_GRID;
   return BAK_VARIANT_STREAM;
 }

@@ -120,8 +120,6 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   long long ph_last = clock64();
 #endif
   constexpr int kMaxWarps = MAXNT / 32;
-  // third register buffer (pull x_{t+2} before the arithmetic) when it fits
-  constexpr bool kEarly = E * sizeof(T) <= 64;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NT = static_cast<int>(blockDim.x) - 32;  // consumers; the last warp produces
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
@@ -231,7 +229,12 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     int ls = 0;        // stage of the next step to pull into registers
     uint32_t lph = 0;  // its phase parity
 
-    // stage -> registers (pad rows beyond obs read as 0); returns the stage index
+    // stage -> registers (pad rows beyond obs read as 0); returns the stage index.
+    // 32-bit shared addresses; the unmasked path is taken when this thread's E rows
+    // are all inside the system (every CTA but the ragged last one).
+    const bool full_rows = kv == E;
+    const uint32_t xs_base = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
+    const uint32_t stage_bytes = static_cast<uint32_t>(prm.stage_elems * sizeof(T));
     auto pull = [&](T* xr, int64_t& c, T& n2, T& rinv) -> int {
       if (!mbar_test(&full[ls], lph)) {
         const uint64_t t0 = globaltimer();
@@ -246,9 +249,14 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
       c = meta[ls].col;
       n2 = static_cast<T>(meta[ls].n2);
       rinv = static_cast<T>(meta[ls].rinv);
-      const T* X = xs + static_cast<size_t>(ls) * prm.stage_elems;
+      const uint32_t a0 = xs_base + static_cast<uint32_t>(ls) * stage_bytes;
+      if (full_rows) {
 #pragma unroll
-      for (int k = 0; k < E; ++k) xr[k] = (k < kv) ? X[tid + k * NT] : T(0);
+        for (int k = 0; k < E; ++k) xr[k] = lds<T>(a0 + static_cast<uint32_t>(k * NT * sizeof(T)));
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) xr[k] = (k < kv) ? lds<T>(a0 + static_cast<uint32_t>(k * NT * sizeof(T))) : T(0);
+      }
       const int got = ls;
       if (++ls == S) { ls = 0; lph ^= 1u; }
       return got;
@@ -439,17 +447,15 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     T a0 = upd_warp ? ag[c0] : T(0);
     T a1 = (upd_warp && total > 1) ? ag[c1] : T(0);
 
-    constexpr int EQ = kEarly ? E : 1;
-    T xq[EQ];
     int64_t sweep = 0, k = 0, t = 0;
     bool converged = false;
-    while (!aborted) {
+    // one column step: update with xc (column t), dot with xn (column t+1), then
+    // refill xc with column t+2 (its LDS latency overlaps the reduction).
+    // Returns true when the solve ends.  Called with the two buffers swapped on
+    // alternate steps, so no register copies.
+    auto step = [&](T (&xc)[E], T (&xn)[E]) -> bool {
       PH(7);
       const bool more = t + 2 < total;
-      int64_t c2 = c1;
-      T n2_2 = n2_1, ri_2 = ri_1;
-      int sp = -1;
-      if (kEarly && more) sp = pull(xq, c2, n2_2, ri_2);
       const T d = quotient(P, n2_0, ri_0);
       PH(0);
       const bool last = (k == ncols - 1);
@@ -468,14 +474,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         qv = Num<T>::add(Num<T>::add(qa[0], qa[1]), Num<T>::add(qa[2], qa[3]));
       }
       PH(1);
-#pragma unroll
-      for (int kk = 0; kk < E; ++kk) xc[kk] = xn[kk];
-      if (kEarly) {
-#pragma unroll
-        for (int kk = 0; kk < E; ++kk) xn[kk] = xq[kk < EQ ? kk : 0];
-      } else if (more) {
-        sp = pull(xn, c2, n2_2, ri_2);
-      }
+      int64_t c2 = c1;
+      T n2_2 = n2_1, ri_2 = ri_1;
+      const int sp = more ? pull(xc, c2, n2_2, ri_2) : -1;
       PH(2);
       if (upd_warp) {
         const T na = Num<T>::add(a0, d);
@@ -483,17 +484,16 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         a0 = (c1 == c0) ? na : a1;
         if (more) a1 = ag[c2];  // store->load order in one thread: never stale
       }
-      aborted = reduce(pv, qv, last, rc++, sp, -1, P, Q);
+      if (reduce(pv, qv, last, rc++, sp, -1, P, Q)) return true;
       PH(6);
-      if (aborted) break;
       if (last) {
         if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
         ++sweep;
         if (prm.thresh2 >= 0.0 && static_cast<double>(Q) <= prm.thresh2) {
           converged = true;
-          break;
+          return true;
         }
-        if (sweep == prm.max_iter) break;
+        if (sweep == prm.max_iter) return true;
         k = 0;
       } else {
         ++k;
@@ -505,6 +505,13 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
       c1 = c2;
       n2_1 = n2_2;
       ri_1 = ri_2;
+      return false;
+    };
+    if (!aborted) {
+      while (true) {
+        if (step(xc, xn)) break;
+        if (step(xn, xc)) break;
+      }
     }
 
 #pragma unroll
@@ -631,34 +638,32 @@ static bool plan_env(int dtype, int variant, int64_t obs, SweepPlan& pl) {
 bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
   const int sms = device_sms();
   if (plan_env(dtype, variant, obs, pl)) return true;
-  const int max_e = dtype == BAK_F64 ? 8 : 16;
+  // Measured on B200 (tools/tune2.sh): E = 8 rows per thread and as few warps
+  // per CTA as possible; grow the cluster (single-warp CTAs) before warps.
+  const int e0 = 8;
   if (variant == BAK_VARIANT_CTA) {
-    // short columns: a single warp when E stays small, else the fewest warps
-    for (int e : kEs) {
-      if (e > 2 * max_e) break;
-      if (static_cast<int64_t>(32) * e >= obs && plan_fill(dtype, variant, obs, 32, e, 1, pl, 4)) return true;
-    }
-    for (int e : kEs) {
-      if (e > max_e) break;
+    for (int e : {e0, 16, 32, 4, 2, 1}) {
       const int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
       if (nt <= 256 && plan_fill(dtype, variant, obs, nt, e, 1, pl, 4)) return true;
-    }
-    for (int e : kEs) {
-      const int nt = static_cast<int>(round_up((obs + e - 1) / e, 32));
-      if (plan_fill(dtype, variant, obs, nt, e, 1, pl, 2)) return true;
     }
     return false;
   }
   if (variant == BAK_VARIANT_CLUSTER) {
-    for (int c : {2, 4, 8, 16}) {
-      const int64_t per = (obs + c - 1) / c;
-      for (int e : kEs) {
-        if (e > max_e) break;
-        const int nt = static_cast<int>(round_up((per + e - 1) / e, 32));
-        if (nt > 128) continue;
-        int parts = static_cast<int>((obs + static_cast<int64_t>(nt) * e - 1) / (static_cast<int64_t>(nt) * e));
-        if (parts < 2) parts = 2;
-        if (plan_fill(dtype, variant, obs, nt, e, parts, pl, 4)) return true;
+    for (int nt : {32, 64, 128, 256}) {
+      for (int e : {e0, 16, 4, 2, 1}) {
+        const int64_t rows = static_cast<int64_t>(nt) * e;
+        int c = static_cast<int>((obs + rows - 1) / rows);
+        if (c < 2) c = 2;
+        int cp = 2;
+        while (cp < c) cp *= 2;
+        if (cp > kMaxCluster) continue;
+        // shrink rows per CTA so that the cluster's CTAs share the rows evenly
+        const int64_t per = (obs + cp - 1) / cp;
+        const int nt2 = static_cast<int>(round_up((per + e - 1) / e, 32));
+        if (plan_fill(dtype, variant, obs, nt2, e, static_cast<int>((obs + static_cast<int64_t>(nt2) * e - 1) /
+                                                                   (static_cast<int64_t>(nt2) * e)),
+                      pl, 4))
+          return true;
       }
     }
     return false;

@@ -122,6 +122,16 @@ int bak_gram_solve(int dtype, int64_t vars, const double* gpart, const double* s
                    int64_t cols_stride, const void* norms2, const double* G, void* a, double* delta,
                    double* history, int64_t* ctrl, int64_t* status, void* stream);
 
+/* One call for the GRAM variant: G = X^T X (norms2_out = diag G, in T), all
+ * sweeps (zero-norm columns skipped in the solve), and - when thresh2 < 0 and
+ * resid != NULL - the final residual y - x a fused into the last pass
+ * (status[3] == BAK_VARIANT_GRAM | 256 then).  Synchronizes once (zero-norm
+ * check, bak.py:186-187 -> BAK_EINVAL). */
+int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, const void* y,
+                   const int32_t* cols, int64_t ncols, int64_t cols_stride, void* norms2_out, void* e,
+                   void* a, int64_t max_iter, double thresh2, double* history, int64_t* status,
+                   void* resid, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---- (4) batched many-small-systems solve ---------------------------------
  * One CTA per system; each CTA runs the whole solve_bak (bak.py:146-195) for
  * its system: e = y (or y - x a0), sweeps, early break, final residual and drift.

@@ -44,6 +44,8 @@ SIGNATURES = {
     "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
     "bak_gram_solve": (_int, [_int, _i64, _vp, _vp, _i64, _i64, _i64, _dbl, _vp, _i64, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),
+    "bak_solve_gram": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _vp,
+                              _vp, _vp, _vp, _i64, _vp]),
     "bak_mailbox_bytes": (_i64, [_i64]),
     "bak_sweep_rowshard": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _vp, _vp, _int, _int,
                                   _vp, _i64, _int, _vp, _i64, _vp]),

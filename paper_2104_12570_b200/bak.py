@@ -275,6 +275,9 @@ def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto
         a = torch.zeros(nv, dtype=yd.dtype, device=dev)
     thresh2 = cfg.tol * cfg.tol * ynorm2 if cfg.tol > 0 else -1.0   # bak.py:182
 
+    if variant == "gram":
+        return _solve_gram(lib, torch, dm, yd, a, a0, cfg, ynorm2, thresh2, ws, st, t0, return_device)
+
     norms = colnorms(dm, ws)
     norms_h = norms.cpu().numpy()
     if not norms_h.any():
@@ -344,6 +347,54 @@ def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto
         drift_warning=bool(drift_rel > DRIFT_TOL),
         variant=_lib.VARIANT_NAMES.get(used, str(used)),
     )
+
+
+def _solve_gram(lib, torch, dm, yd, a, a0, cfg, ynorm2, thresh2, ws, st, t0, return_device):
+    """variant="gram": one C call (bak_solve_gram) — G and norms, the sweeps
+    (one pass over x each), and, without early break, the final residual
+    fused into the last pass."""
+    dev = dm.data.device
+    obs, nv, code = dm.obs, dm.vars, dm.code
+    e = torch.empty_like(yd)
+    if a0 is not None:
+        _residual(lib, dm, a, yd, e, ws, st)            # e = y - x a0 (bak.py:189)
+    else:
+        e.copy_(yd)
+    norms = torch.empty(nv, dtype=yd.dtype, device=dev)
+    hist = torch.zeros(cfg.max_iter, dtype=torch.float64, device=dev) if cfg.record_history else None
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    resid = torch.empty_like(yd)
+    if cfg.ordering == "cyclic":
+        cols, ncols, stride = None, nv, 0
+    else:
+        perms = _permutation_chunks(cfg.ordering_seed, nv, None)
+        block = np.stack([next(perms) for _ in range(cfg.max_iter)]).astype(np.int32)
+        cols = torch.from_numpy(block).to(dev)
+        ncols, stride = nv, nv
+    rc = lib.bak_solve_gram(code, dm.ptr, obs, nv, dm.ldx, _ptr(yd), _ptr(cols), ncols, stride, _ptr(norms), _ptr(e),
+                            _ptr(a), cfg.max_iter, thresh2, _ptr(hist), _ptr(status), _ptr(resid), ws.ptr, ws.nbytes,
+                            st)
+    if rc == 1 and b"zero norm" in lib.bak_last_error():
+        raise ValueError("every column of x has zero norm; nothing to solve")
+    _lib.check(rc, "bak_solve_gram")
+    stat = status.cpu().numpy()
+    if int(stat[2]):
+        raise _lib.BakError(f"bak_solve_gram device error {int(stat[2])}")
+    sweeps, converged = int(stat[0]), bool(stat[1])
+    if not (int(stat[3]) & 256):                         # residual not fused (early break possible)
+        _residual(lib, dm, a, yd, resid, ws, st)         # bak.py:130
+    drift2 = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.check(lib.bak_diff_norm2(code, _ptr(e), _ptr(resid), obs, _ptr(drift2), ws.ptr, ws.nbytes, st),
+               "bak_diff_norm2")
+    drift = float(np.sqrt(drift2.item()))
+    wall = time.perf_counter() - t0
+    drift_rel = drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny)
+    return SolveReport(
+        a_hat=a if return_device else a.cpu().numpy(),
+        residual=resid if return_device else resid.cpu().numpy(),
+        residual_norm_history=hist[:sweeps].cpu().tolist() if hist is not None else None,
+        sweeps_run=sweeps, converged=converged, wall_time=wall, drift_warning=bool(drift_rel > DRIFT_TOL),
+        variant="gram")
 
 
 def residual_norm(e) -> float:

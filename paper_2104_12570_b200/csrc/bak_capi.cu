@@ -14,6 +14,8 @@ static thread_local char g_err[512] = "";
 static std::atomic<int64_t> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+void g_err_clear() { g_err[0] = 0; }
+
 void set_error(const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);

@@ -199,6 +199,7 @@ __device__ __forceinline__ void report_error(int64_t* status, int64_t code) {
 // ---------------- host side ----------------
 namespace bak {
 void set_error(const char* fmt, ...);
+void g_err_clear();
 int cuda_fail(cudaError_t err, const char* what);
 inline size_t dtype_size(int dtype) { return dtype == BAK_F64 ? 8 : 4; }
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }

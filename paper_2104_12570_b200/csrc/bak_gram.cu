@@ -19,6 +19,7 @@
 // rows), are used for both the update and the dot, and the next tile's values
 // are prefetched while the current one is reduced.
 #include <cstdio>
+#include <vector>
 
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
@@ -223,10 +224,14 @@ __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p)
     const double gcol = gnext;
     if (tid < V && kk + 1 < p.ncols) gnext = p.G[static_cast<int64_t>(ord[kk + 1]) * V + tid];
     if (tid == j) {
-      const T d = Num<T>::div(static_cast<T>(rj), static_cast<T>(n2s[j]));
-      dsh[kk & 1] = static_cast<double>(d);
-      dj = static_cast<double>(d);
-      aj = Num<T>::add(aj, d);
+      if (n2s[j] != 0.0) {
+        const T d = Num<T>::div(static_cast<T>(rj), static_cast<T>(n2s[j]));
+        dsh[kk & 1] = static_cast<double>(d);
+        dj = static_cast<double>(d);
+        aj = Num<T>::add(aj, d);
+      } else {
+        dsh[kk & 1] = 0.0;  // zero-norm column: skipped, coefficient frozen (bak.py:101-103)
+      }
     }
     __syncthreads();
     if (tid < V) rj = __fma_rn(-gcol, dsh[kk & 1], rj);
@@ -404,5 +409,110 @@ extern "C" int bak_gram_solve(int dtype, int64_t vars, const double* gpart, cons
     gram_solve_kernel<float><<<1, 512, 0, st>>>(sp);
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
+  return BAK_OK;
+}
+
+// One call: G (+ norms from its diagonal), then the GRAM sweeps; zero-norm columns
+// are skipped in the solve; with thresh2 < 0 and resid != NULL the final pass
+// also writes resid = y - x a (fused; no separate residual pass over x).
+extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, const void* y,
+                              const int32_t* cols, int64_t ncols, int64_t cols_stride, void* norms2_out, void* e,
+                              void* a, int64_t max_iter, double thresh2, double* history, int64_t* status,
+                              void* resid, void* workspace, int64_t workspace_bytes, void* stream) {
+  g_err_clear();
+  if ((dtype != BAK_F32 && dtype != BAK_F64) || obs < 1 || !gram_supported(vars) || ldx < obs || !x || !norms2_out ||
+      !e || !a || !status || max_iter < 1 || (!cols && ncols != vars) || (resid && !y)) {
+    set_error("bak_solve_gram: bad arguments");
+    return BAK_EINVAL;
+  }
+  const size_t ts = dtype_size(dtype);
+  if (reinterpret_cast<uintptr_t>(x) % 16 || (ldx * static_cast<int64_t>(ts)) % 16) {
+    set_error("bak_solve_gram: x must be 16-byte aligned with ldx*sizeof(T) %% 16 == 0");
+    return BAK_EINVAL;
+  }
+  if (workspace_bytes < gram_workspace_bytes(dtype, obs, vars)) {
+    set_error("bak_solve_gram: workspace too small (need %lld)", (long long)gram_workspace_bytes(dtype, obs, vars));
+    return BAK_EWORKSPACE;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nblk = gram_nblk();
+  char* w = static_cast<char*>(workspace);
+  double* G = reinterpret_cast<double*>(w);
+  w += vars * vars * 8;
+  double* gpart = reinterpret_cast<double*>(w);
+  w += nblk * vars * 8;
+  double* sqpart = reinterpret_cast<double*>(w);
+  w += nblk * 8;
+  double* delta = reinterpret_cast<double*>(w);
+  w += vars * 8;
+  GramCtrl* ctrl = reinterpret_cast<GramCtrl*>(w);
+  w += 64;
+  double* gparts_ws = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
+  const int64_t gparts_bytes = workspace_bytes - (reinterpret_cast<char*>(gparts_ws) - static_cast<char*>(workspace));
+  BAK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int64_t), st));
+  if (int rc = launch_gram_g(dtype, x, obs, ldx, vars, G, gparts_ws, gparts_bytes, st, norms2_out)) return rc;
+  // all-zero matrix -> the reference's ValueError (bak.py:186-187)
+  {
+    std::vector<unsigned char> h(static_cast<size_t>(vars) * ts);
+    BAK_CHECK_CUDA(cudaMemcpyAsync(h.data(), norms2_out, h.size(), cudaMemcpyDeviceToHost, st));
+    BAK_CHECK_CUDA(cudaStreamSynchronize(st));
+    bool any = false;
+    for (int64_t j = 0; j < vars && !any; ++j)
+      any = dtype == BAK_F64 ? reinterpret_cast<double*>(h.data())[j] != 0.0
+                             : reinterpret_cast<float*>(h.data())[j] != 0.0f;
+    if (!any) {
+      set_error("every column of x has zero norm; nothing to solve");
+      return BAK_EINVAL;
+    }
+  }
+  BAK_CHECK_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(GramCtrl), st));
+  const bool use_tma = gram_tma_supported(vars);
+  SolveParams sp{vars, use_tma ? gram_tma_grid(dtype) : nblk, 0, max_iter, thresh2, cols, ncols, cols_stride,
+                 norms2_out, G, gpart, sqpart, a, delta, history, ctrl, status};
+  PassParams pp{x, obs, ldx, vars, e, delta, 0, 1, gpart, sqpart, ctrl};
+  const bool fuse_resid = resid && thresh2 < 0.0 && use_tma;
+  auto pass = [&](int apply, int dot, bool final_pass) -> int {
+    if (use_tma)
+      return launch_gram_pass_tma(dtype, x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart, &ctrl->done, st,
+                                  final_pass && fuse_resid ? a : nullptr, y, resid);
+    pp.apply = apply;
+    pp.dot = dot;
+    if (dtype == BAK_F64)
+      gram_pass_kernel<double><<<static_cast<unsigned>(nblk), kGT, 0, st>>>(pp);
+    else
+      gram_pass_kernel<float><<<static_cast<unsigned>(nblk), kGT, 0, st>>>(pp);
+    count_launches(1);
+    BAK_CHECK_CUDA(cudaGetLastError());
+    return BAK_OK;
+  };
+  auto solve = [&](int64_t s) -> int {
+    sp.sweep = s;
+    if (dtype == BAK_F64)
+      gram_solve_kernel<double><<<1, 512, 0, st>>>(sp);
+    else
+      gram_solve_kernel<float><<<1, 512, 0, st>>>(sp);
+    count_launches(1);
+    BAK_CHECK_CUDA(cudaGetLastError());
+    return BAK_OK;
+  };
+  int rc = pass(0, 1, false);
+  if (rc) return rc;
+  for (int64_t s = 1; s <= max_iter; ++s) {
+    if ((rc = solve(s))) return rc;
+    if ((rc = pass(1, s < max_iter ? 1 : 0, s == max_iter))) return rc;
+    if (thresh2 >= 0.0 && s % 16 == 0) {
+      int64_t done = 0;
+      BAK_CHECK_CUDA(cudaMemcpyAsync(&done, &ctrl->done, sizeof(done), cudaMemcpyDeviceToHost, st));
+      BAK_CHECK_CUDA(cudaStreamSynchronize(st));
+      if (done) break;
+    }
+  }
+  if ((rc = solve(max_iter + 1))) return rc;
+  // status[2] stays 0; bit 8 of status[3] tells the caller the residual was fused
+  if (fuse_resid) {
+    const int64_t v = BAK_VARIANT_GRAM | 256;
+    BAK_CHECK_CUDA(cudaMemcpyAsync(status + 3, &v, sizeof(v), cudaMemcpyHostToDevice, st));
+    BAK_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
   return BAK_OK;
 }

@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
 }
 
 // G (vars x vars, full, symmetric) = sum over chunks of the lower block partials
+template <typename T>
 __global__ void gram_reduce_kernel(const double* __restrict__ part, int nchunks, int nb, int64_t V,
-                                   double* __restrict__ G) {
+                                   double* __restrict__ G, T* __restrict__ norms) {
   const int nblk = nb * (nb + 1) / 2;
   const int blk = blockIdx.y;
   int bi = 0;
@@ -165,6 +166,7 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nchunks,
     for (int c = 0; c < nchunks; ++c) s += part[(static_cast<size_t>(c) * nblk + blk) * kBT * kBT + e];
     G[gj * V + gi] = s;  // column-major (gi, gj)
     G[gi * V + gj] = s;  // mirror (gj, gi)
+    if (norms && gi == gj) norms[gi] = static_cast<T>(s);  // n2_j = G_jj (fp64-accumulated)
   }
 }
 
@@ -184,7 +186,7 @@ int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk
 }
 
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
-                  int64_t part_bytes, cudaStream_t st) {
+                  int64_t part_bytes, cudaStream_t st, void* norms_out) {
   int nchunks;
   int64_t chunk;
   const int64_t need = gram_g_workspace(obs, vars, nchunks, chunk);
@@ -209,7 +211,12 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   }
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
-  gram_reduce_kernel<<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), nchunks, nb, vars, G);
+  if (dtype == BAK_F64)
+    gram_reduce_kernel<double><<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), nchunks, nb, vars,
+                                                               G, static_cast<double*>(norms_out));
+  else
+    gram_reduce_kernel<float><<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), nchunks, nb, vars,
+                                                              G, static_cast<float*>(norms_out));
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;

@@ -32,6 +32,9 @@ struct TmaPassParams {
   double* gpart;
   double* sqpart;
   const int64_t* done;
+  const void* afin;  // non-null: also write resid = y - x @ afin (fused final residual, bak.py:130)
+  const void* y;
+  void* resid;
 };
 
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -65,6 +68,9 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
   double* dsh = reinterpret_cast<double*>(empty + kS);  // [VB]
   double* red = dsh + VB;                                // [kWarps][kR]
   double* es = red + kWarps * kR;                        // [kR]
+  double* ash = es + kR;                                 // [VB] final coefficients (fused residual)
+  double* red2 = ash + VB;                               // [kWarps][kR]
+  const bool want_r = p.afin != nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = static_cast<int>(p.vars);
   if (tid == 0) {
@@ -74,7 +80,10 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
     }
     fence_mbar_init();
   }
-  for (int j = tid; j < VB; j += blockDim.x) dsh[j] = (p.apply && j < V) ? p.delta[j] : 0.0;
+  for (int j = tid; j < VB; j += blockDim.x) {
+    dsh[j] = (p.apply && j < V) ? p.delta[j] : 0.0;
+    ash[j] = (want_r && j < V) ? static_cast<double>(static_cast<const T*>(p.afin)[j]) : 0.0;
+  }
   __syncthreads();
 
   if (warp == kWarps) {
@@ -106,17 +115,22 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
   uint32_t ph = 0;
   int prev = -1;
   int64_t tile = blockIdx.x;
-  T e_next = T(0);
+  T e_next = T(0), y_next = T(0);
+  const T* yv = static_cast<const T*>(p.y);
+  T* rv = static_cast<T*>(p.resid);
   if (warp == 0 && tile < p.ntiles) {
     const int64_t row = tile * kR + lane;
     e_next = row < p.obs ? e[row] : T(0);
+    if (want_r) y_next = row < p.obs ? yv[row] : T(0);
   }
   for (; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row = tile * kR + lane;
-    const T e_cur = e_next;
+    const T e_cur = e_next, y_cur = y_next;
     if (warp == 0) {
       const int64_t nrow = (tile + gridDim.x) * kR + lane;
-      e_next = (tile + gridDim.x < p.ntiles && nrow < p.obs) ? e[nrow] : T(0);
+      const bool nok = tile + gridDim.x < p.ntiles && nrow < p.obs;
+      e_next = nok ? e[nrow] : T(0);
+      if (want_r) y_next = nok ? yv[nrow] : T(0);
     }
     {
       const uint64_t t0 = globaltimer();
@@ -129,6 +143,12 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
 #pragma unroll
       for (int q = 0; q < CW; ++q) t = __fma_rn(static_cast<double>(X[q * kR]), dsh[warp * CW + q], t);
       red[warp * kR + lane] = t;
+    }
+    if (want_r) {
+      double t2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < CW; ++q) t2 = __fma_rn(static_cast<double>(X[q * kR]), ash[warp * CW + q], t2);
+      red2[warp * kR + lane] = t2;
     }
     bar_cons();
     if (tid == 0 && prev >= 0) mbar_arrive1(&empty[prev]);  // previous tile fully consumed
@@ -144,6 +164,12 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
         sq = __fma_rn(ev, ev, sq);
       }
       es[lane] = ev;
+      if (want_r && row < p.obs) {
+        double r2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < kWarps; ++c) r2 += red2[c * kR + lane];
+        rv[row] = static_cast<T>(static_cast<double>(y_cur) - r2);
+      }
     }
     bar_cons();
     if (p.dot) {
@@ -186,7 +212,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <typename T, int CW>
 int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStream_t st) {
   constexpr int VB = CW * kWarps;
-  const size_t smem = kS * static_cast<size_t>(kR) * VB * sizeof(T) + 2 * kS * 8 + VB * 8 + kWarps * kR * 8 + kR * 8;
+  const size_t smem = kS * static_cast<size_t>(kR) * VB * sizeof(T) + 2 * kS * 8 + 2 * VB * 8 + 2 * kWarps * kR * 8 +
+                      kR * 8;
   auto kern = gram_pass_tma_kernel<T, CW>;
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<grid, kCons + 32, smem, st>>>(map, p);
@@ -204,7 +231,7 @@ int gram_tma_grid(int dtype) { return (dtype == BAK_F32 ? 2 : 1) * device_sms();
 // x: column-major obs x vars, ldx*sizeof(T) % 16 == 0
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
                          const double* delta, int apply, int dot, double* gpart, double* sqpart, const int64_t* done,
-                         cudaStream_t st) {
+                         cudaStream_t st, const void* afin, const void* y, void* resid) {
   auto enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -225,7 +252,7 @@ int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int
     set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
     return BAK_ECUDA;
   }
-  TmaPassParams p{obs, vars, (obs + kR - 1) / kR, e, delta, apply, dot, gpart, sqpart, done};
+  TmaPassParams p{obs, vars, (obs + kR - 1) / kR, e, delta, apply, dot, gpart, sqpart, done, afin, y, resid};
   const int grid = gram_tma_grid(dtype);
   if (dtype == BAK_F64) {
     if (cw == 8) return launch_cw<double, 8>(map, p, grid, st);

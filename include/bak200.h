@@ -117,6 +117,10 @@ int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t
 int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                   const double* delta, int apply, int dot, double* gpart, double* sqpart,
                   const int64_t* done_flag, void* stream);
+/* bak_gram_pass + (afin != NULL) resid = y - x @ afin fused into the same pass. */
+int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
+                        const double* delta, int apply, int dot, double* gpart, double* sqpart,
+                        const int64_t* done_flag, const void* afin, const void* y, void* resid, void* stream);
 int bak_gram_solve(int dtype, int64_t vars, const double* gpart, const double* sqpart, int64_t nparts,
                    int64_t sweep, int64_t max_iter, double thresh2, const int32_t* cols, int64_t ncols,
                    int64_t cols_stride, const void* norms2, const double* G, void* a, double* delta,
@@ -166,6 +170,12 @@ int bak_sweep_rowshard(int dtype,
                        int rank, int nranks, void* const* mailboxes, int64_t epoch_base,
                        int nranks_local,
                        void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Plumbing: rows [r0, r0+rows) of a column-major host matrix (leading dim sld,
+ * element size elem) to the same rows of a device matrix (leading dim dld);
+ * one cudaMemcpy2DAsync (pinned source => overlaps kernels on other streams). */
+int bak_copy_rows_h2d(void* dst, int64_t dld, const void* src, int64_t sld, int64_t r0, int64_t rows,
+                      int64_t vars, int64_t elem, void* stream);
 
 /* Peer mapping helpers for one-process-per-GPU (CUDA IPC; 64-byte handles). */
 int bak_ipc_get_handle(void* devptr, void* handle64);

@@ -42,6 +42,9 @@ SIGNATURES = {
     "bak_gram_matrix_workspace": (_i64, [_int, _i64, _i64]),
     "bak_gram_matrix": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
+    "bak_gram_pass_resid": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,
+                                   _vp, _vp]),
+    "bak_copy_rows_h2d": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp]),
     "bak_gram_solve": (_int, [_int, _i64, _vp, _vp, _i64, _i64, _i64, _dbl, _vp, _i64, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),
     "bak_solve_gram": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _vp,

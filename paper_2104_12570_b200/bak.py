@@ -249,6 +249,8 @@ def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto
     lib = _lib.load()
     if variant not in _lib.VARIANTS:
         raise ValueError(f"unknown variant {variant!r}, expected one of {tuple(_lib.VARIANTS)}")
+    if variant == "gram" and _pipelinable(torch, x):
+        return _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device)
     dm = to_device_matrix(x, device)
     dev = dm.data.device
     obs, nv, code = dm.obs, dm.vars, dm.code
@@ -394,6 +396,147 @@ def _solve_gram(lib, torch, dm, yd, a, a0, cfg, ynorm2, thresh2, ws, st, t0, ret
         residual=resid if return_device else resid.cpu().numpy(),
         residual_norm_history=hist[:sweeps].cpu().tolist() if hist is not None else None,
         sweeps_run=sweeps, converged=converged, wall_time=wall, drift_warning=bool(drift_rel > DRIFT_TOL),
+        variant="gram")
+
+
+_PIPE_MIN_BYTES = 256 << 20
+_PIPE_CHUNK_BYTES = 1 << 30
+
+
+def _pipelinable(torch, x):
+    """Large PINNED host x (torch CPU tensor, column-major view): upload in row
+    blocks overlapped with the first GPU work (G and the first pass)."""
+    return (_is_torch(x) and not x.is_cuda and x.ndim == 2 and x.is_pinned() and x.stride(0) == 1
+            and x.dtype in (torch.float32, torch.float64) and x.numel() * x.element_size() >= _PIPE_MIN_BYTES
+            and x.shape[1] <= 256)
+
+
+def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
+    """variant="gram" from a pinned host matrix: row blocks of x are copied on
+    two copy streams (cudaMemcpy2DAsync) while the compute stream builds each
+    block's G partial and first-pass partials; sweeps 1.. run over the whole
+    device matrix.  Same results as the resident path (partials summed in
+    block order)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    obs, nv = x.shape
+    np_dtype = np.float64 if x.dtype == torch.float64 else np.float32
+    ts = 8 if np_dtype == np.float64 else 4
+    code = _dtype_code(np_dtype)
+    ld = _aligned_ld(obs, ts)
+    sld = x.stride(1)
+    data = torch.empty((nv, ld), dtype=x.dtype, device=dev)
+    dm = DeviceMatrix(data, obs, nv, np_dtype)
+    yd = _to_device_vector(y, np_dtype, dev)
+    if yd.shape[0] != obs:
+        raise ValueError(f"y has length {yd.shape[0]}, expected {obs}")
+    main = torch.cuda.current_stream(dev)
+    st = ctypes.c_void_p(main.cuda_stream)
+    t0 = time.perf_counter()
+    # row blocks (multiples of 32 rows: whole TMA tiles), two copy engines
+    rows_chunk = max(32, (_PIPE_CHUNK_BYTES // (nv * ts)) // 32 * 32)
+    blocks = [(r0, min(obs, r0 + rows_chunk)) for r0 in range(0, obs, rows_chunk)]
+    copy_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    for cs in copy_streams:
+        cs.wait_stream(main)
+    events = []
+    for i, (r0, r1) in enumerate(blocks):
+        cs = copy_streams[i % 2]
+        _lib.check(lib.bak_copy_rows_h2d(dm.ptr, ld, ctypes.c_void_p(x.data_ptr()), sld, r0, r1 - r0, nv, ts,
+                                         ctypes.c_void_p(cs.cuda_stream)), "bak_copy_rows_h2d")
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        events.append(ev)
+    wsb = max(lib.bak_gram_matrix_workspace(code, rows_chunk, nv), lib.bak_residual_workspace(code, obs, nv),
+              lib.bak_colnorms_workspace(code, obs, 1), 1 << 16)
+    ws = _Workspace(torch, dev, wsb)
+    ynorm2 = float(_sumsq(lib, torch, code, yd, ws, st).item())
+    if ynorm2 == 0.0:
+        for ev in events:
+            main.wait_event(ev)
+        a_z = torch.zeros(nv, dtype=yd.dtype, device=dev)
+        r_z = torch.zeros(obs, dtype=yd.dtype, device=dev)
+        return SolveReport(a_z if return_device else a_z.cpu().numpy(), r_z if return_device else r_z.cpu().numpy(),
+                           [] if cfg.record_history else None, 0, True, time.perf_counter() - t0)
+    a = torch.zeros(nv, dtype=yd.dtype, device=dev)
+    if a0 is not None:
+        a = _to_device_vector(a0, np_dtype, dev, "a0").clone()
+        if a.shape[0] != nv:
+            raise ValueError(f"a0 has length {a.shape[0]}, expected {nv}")
+    thresh2 = cfg.tol * cfg.tol * ynorm2 if cfg.tol > 0 else -1.0
+    e = yd.clone()
+    nblk = lib.bak_gram_pass_blocks(code, nv)
+    nb = len(blocks)
+    Gp = torch.empty((nb, nv, nv), dtype=torch.float64, device=dev)
+    gp0 = torch.zeros((nb, nblk, nv), dtype=torch.float64, device=dev)
+    sp0 = torch.zeros((nb, nblk), dtype=torch.float64, device=dev)
+    ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
+    delta = torch.zeros(nv, dtype=torch.float64, device=dev)
+    for i, (r0, r1) in enumerate(blocks):
+        main.wait_event(events[i])
+        xb = ctypes.c_void_p(dm.data.data_ptr() + r0 * ts)
+        _lib.check(lib.bak_gram_matrix(code, xb, r1 - r0, nv, ld, _ptr(Gp[i]), ws.ptr, ws.nbytes, st),
+                   "bak_gram_matrix")
+        if a0 is not None:  # e = y - x a0 on this block (bak.py:189)
+            _lib.check(lib.bak_residual(code, xb, r1 - r0, nv, ld, _ptr(a), ctypes.c_void_p(yd.data_ptr() + r0 * ts),
+                                        ctypes.c_void_p(e.data_ptr() + r0 * ts), ws.ptr, ws.nbytes, st),
+                       "bak_residual")
+        _lib.check(lib.bak_gram_pass(code, xb, r1 - r0, nv, ld, ctypes.c_void_p(e.data_ptr() + r0 * ts), _ptr(delta),
+                                     0, 1, _ptr(gp0[i]), _ptr(sp0[i]), _ptr(ctrl), st), "bak_gram_pass")
+    G = Gp[0].clone()
+    for i in range(1, nb):
+        G += Gp[i]
+    norms = G.diagonal().to(yd.dtype).contiguous()
+    norms_h = norms.cpu().numpy()
+    if not norms_h.any():
+        raise ValueError("every column of x has zero norm; nothing to solve")
+    hist = torch.zeros(cfg.max_iter, dtype=torch.float64, device=dev) if cfg.record_history else None
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    if cfg.ordering == "cyclic":
+        cols, ncols, stride = None, nv, 0
+    else:
+        perms = _permutation_chunks(cfg.ordering_seed, nv, None)
+        block = np.stack([next(perms) for _ in range(cfg.max_iter)]).astype(np.int32)
+        cols = torch.from_numpy(block).to(dev)
+        ncols, stride = nv, nv
+    gpart = torch.zeros((nblk, nv), dtype=torch.float64, device=dev)
+    sqpart = torch.zeros(nblk, dtype=torch.float64, device=dev)
+    resid = torch.empty_like(yd)
+    fused = thresh2 < 0
+
+    def solve(gp, sp, sweep):
+        _lib.check(lib.bak_gram_solve(code, nv, _ptr(gp), _ptr(sp), sp.numel(), sweep, cfg.max_iter, thresh2,
+                                      _ptr(cols), ncols, stride, _ptr(norms), _ptr(G), _ptr(a), _ptr(delta),
+                                      _ptr(hist), _ptr(ctrl), _ptr(status), st), "bak_gram_solve")
+
+    def full_pass(dot, last):
+        afin = a if (last and fused) else None
+        _lib.check(lib.bak_gram_pass_resid(code, dm.ptr, obs, nv, ld, _ptr(e), _ptr(delta), 1, dot, _ptr(gpart),
+                                           _ptr(sqpart), _ptr(ctrl), _ptr(afin), _ptr(yd if afin is not None else None),
+                                           _ptr(resid if afin is not None else None), st), "bak_gram_pass")
+
+    gp, sp = gp0.reshape(-1), sp0.reshape(-1)
+    for sweep in range(1, cfg.max_iter + 1):
+        solve(gp, sp, sweep)
+        full_pass(1 if sweep < cfg.max_iter else 0, sweep == cfg.max_iter)
+        gp, sp = gpart.reshape(-1), sqpart
+        if thresh2 >= 0 and sweep % 16 == 0 and int(ctrl[0].item()):
+            break
+    solve(gp, sp, cfg.max_iter + 1)
+    stat = status.cpu().numpy()
+    sweeps, converged = int(stat[0]), bool(stat[1])
+    if not fused:
+        _residual(lib, dm, a, yd, resid, ws, st)
+    drift2 = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.check(lib.bak_diff_norm2(code, _ptr(e), _ptr(resid), obs, _ptr(drift2), ws.ptr, ws.nbytes, st),
+               "bak_diff_norm2")
+    drift = float(np.sqrt(drift2.item()))
+    wall = time.perf_counter() - t0
+    return SolveReport(
+        a_hat=a if return_device else a.cpu().numpy(),
+        residual=resid if return_device else resid.cpu().numpy(),
+        residual_norm_history=hist[:sweeps].cpu().tolist() if hist is not None else None,
+        sweeps_run=sweeps, converged=converged, wall_time=wall,
+        drift_warning=bool(drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny) > DRIFT_TOL),
         variant="gram")
 
 

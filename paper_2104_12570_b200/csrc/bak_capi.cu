@@ -158,3 +158,18 @@ extern "C" int bak_sweep(int dtype, int variant, const void* x, int64_t obs, int
   set_error("bak_sweep: variant %d not available", variant);
   return BAK_EUNSUPPORTED;
 }
+
+// Row-block host->device copy of a column-major matrix (pipelined uploads):
+// rows [r0, r0+rows) of every column, one 2-D copy (rows*elem bytes x vars).
+extern "C" int bak_copy_rows_h2d(void* dst, int64_t dld, const void* src, int64_t sld, int64_t r0, int64_t rows,
+                                 int64_t vars, int64_t elem, void* stream) {
+  if (!dst || !src || rows < 0 || vars < 1 || elem < 1 || dld < r0 + rows || sld < r0 + rows) {
+    set_error("bak_copy_rows_h2d: bad arguments");
+    return BAK_EINVAL;
+  }
+  if (rows == 0) return BAK_OK;
+  BAK_CHECK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + r0 * elem, dld * elem,
+                                   static_cast<const char*>(src) + r0 * elem, sld * elem, rows * elem, vars,
+                                   cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+  return BAK_OK;
+}

@@ -369,17 +369,35 @@ extern "C" int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t va
   return launch_gram_g(dtype, x, obs, ldx, vars, G, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
+                                   const double* delta, int apply, int dot, double* gpart, double* sqpart,
+                                   const int64_t* done_flag, const void* afin, const void* y, void* resid,
+                                   void* stream);
+
 extern "C" int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                              const double* delta, int apply, int dot, double* gpart, double* sqpart,
                              const int64_t* done_flag, void* stream) {
+  return bak_gram_pass_resid(dtype, x, obs, vars, ldx, e, delta, apply, dot, gpart, sqpart, done_flag, nullptr,
+                             nullptr, nullptr, stream);
+}
+
+extern "C" int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
+                                   const double* delta, int apply, int dot, double* gpart, double* sqpart,
+                                   const int64_t* done_flag, const void* afin, const void* y, void* resid,
+                                   void* stream) {
   if ((dtype != BAK_F32 && dtype != BAK_F64) || obs < 1 || !gram_supported(vars) || ldx < obs || !x || !e ||
-      !delta || !gpart || !sqpart || !done_flag) {
+      !delta || !gpart || !sqpart || !done_flag || (afin && (!y || !resid))) {
     set_error("bak_gram_pass: bad arguments");
     return BAK_EINVAL;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (gram_tma_supported(vars))
-    return launch_gram_pass_tma(dtype, x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart, done_flag, st);
+    return launch_gram_pass_tma(dtype, x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart, done_flag, st, afin,
+                                y, resid);
+  if (afin) {
+    set_error("bak_gram_pass: fused residual needs the TMA pass (vars <= 256)");
+    return BAK_EUNSUPPORTED;
+  }
   PassParams pp{x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart,
                 reinterpret_cast<const GramCtrl*>(done_flag)};
   if (dtype == BAK_F64)

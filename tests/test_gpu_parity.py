@@ -318,3 +318,23 @@ def test_rowsharded_api_stream_single_process():
     ref = orc.solve(x, y, **cfg)
     assert rep.variant == "stream-rowshard"
     assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"], ref_hist=ref["residual_norm_history"])
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_gram_pipelined_host_upload_matches_oracle(precision, monkeypatch):
+    """Pinned host x: row blocks uploaded on two copy streams while G and the
+    first pass run per block; must match the oracle like the resident path."""
+    import torch
+    from paper_2104_12570_b200 import bak as pbak
+    pb = _pb()
+    monkeypatch.setattr(pbak, "_PIPE_MIN_BYTES", 1 << 16)
+    monkeypatch.setattr(pbak, "_PIPE_CHUNK_BYTES", 1 << 20)  # several blocks
+    x, y, _ = orc.config_c3(obs=100_000, nvars=24, precision=precision)
+    hx = torch.from_numpy(np.ascontiguousarray(x.T)).pin_memory().t()  # (obs, vars) column-major, pinned
+    cfg = dict(max_iter=6, tol=0, record_history=True)
+    rep = pb.solve_bak(hx, y, pb.SolveConfig(**cfg), variant="gram")
+    ref = orc.solve(x, y, **cfg)
+    assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"], ref_hist=ref["residual_norm_history"])
+    rep2 = pb.solve_bak(hx, y, pb.SolveConfig(max_iter=80, tol=1e-6), variant="gram")
+    ref2 = orc.solve(x, y, max_iter=80, tol=1e-6)
+    assert rep2.sweeps_run == ref2["sweeps_run"] and rep2.converged == ref2["converged"]

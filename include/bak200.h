@@ -114,6 +114,13 @@ int bak_gram_pass_blocks(int dtype, int64_t vars);
 int64_t bak_gram_matrix_workspace(int dtype, int64_t obs, int64_t vars);
 int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
                     void* workspace, int64_t workspace_bytes, void* stream);
+/* G as bak_gram_matrix plus, fused into the same kernel, the first sweep's
+ * g = X^T e as bak_gram_dot_rows(dtype, obs, vars) partial rows
+ * (g0[r*vars + j], summed in row order by bak_gram_solve); e 16-byte aligned.
+ * Replaces bak_gram_matrix + bak_gram_pass(apply=0, dot=1): one read of x. */
+int64_t bak_gram_dot_rows(int dtype, int64_t obs, int64_t vars);
+int bak_gram_matrix_dot(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
+                        const void* e, double* g0, void* workspace, int64_t workspace_bytes, void* stream);
 int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                   const double* delta, int apply, int dot, double* gpart, double* sqpart,
                   const int64_t* done_flag, void* stream);

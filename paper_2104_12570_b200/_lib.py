@@ -41,6 +41,8 @@ SIGNATURES = {
     "bak_gram_pass_blocks": (_int, [_int, _i64]),
     "bak_gram_matrix_workspace": (_i64, [_int, _i64, _i64]),
     "bak_gram_matrix": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
+    "bak_gram_dot_rows": (_i64, [_int, _i64, _i64]),
+    "bak_gram_matrix_dot": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
     "bak_gram_pass_resid": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,
                                    _vp, _vp]),

@@ -466,22 +466,22 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
     e = yd.clone()
     nblk = lib.bak_gram_pass_blocks(code, nv)
     nb = len(blocks)
+    g0rows = max(lib.bak_gram_dot_rows(code, r1 - r0, nv) for r0, r1 in blocks)
     Gp = torch.empty((nb, nv, nv), dtype=torch.float64, device=dev)
-    gp0 = torch.zeros((nb, nblk, nv), dtype=torch.float64, device=dev)
-    sp0 = torch.zeros((nb, nblk), dtype=torch.float64, device=dev)
+    gp0 = torch.zeros((nb, g0rows, nv), dtype=torch.float64, device=dev)
+    sp0 = torch.zeros((nb, 1), dtype=torch.float64, device=dev)  # unused by the first solve
     ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
     delta = torch.zeros(nv, dtype=torch.float64, device=dev)
     for i, (r0, r1) in enumerate(blocks):
         main.wait_event(events[i])
         xb = ctypes.c_void_p(dm.data.data_ptr() + r0 * ts)
-        _lib.check(lib.bak_gram_matrix(code, xb, r1 - r0, nv, ld, _ptr(Gp[i]), ws.ptr, ws.nbytes, st),
-                   "bak_gram_matrix")
+        eb = ctypes.c_void_p(e.data_ptr() + r0 * ts)
         if a0 is not None:  # e = y - x a0 on this block (bak.py:189)
             _lib.check(lib.bak_residual(code, xb, r1 - r0, nv, ld, _ptr(a), ctypes.c_void_p(yd.data_ptr() + r0 * ts),
-                                        ctypes.c_void_p(e.data_ptr() + r0 * ts), ws.ptr, ws.nbytes, st),
-                       "bak_residual")
-        _lib.check(lib.bak_gram_pass(code, xb, r1 - r0, nv, ld, ctypes.c_void_p(e.data_ptr() + r0 * ts), _ptr(delta),
-                                     0, 1, _ptr(gp0[i]), _ptr(sp0[i]), _ptr(ctrl), st), "bak_gram_pass")
+                                        eb, ws.ptr, ws.nbytes, st), "bak_residual")
+        # this block's G and first-sweep g = X^T e in one read of the block
+        _lib.check(lib.bak_gram_matrix_dot(code, xb, r1 - r0, nv, ld, _ptr(Gp[i]), eb, _ptr(gp0[i]),
+                                           ws.ptr, ws.nbytes, st), "bak_gram_matrix_dot")
     G = Gp[0].clone()
     for i in range(1, nb):
         G += Gp[i]
@@ -504,7 +504,7 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
     fused = thresh2 < 0
 
     def solve(gp, sp, sweep):
-        _lib.check(lib.bak_gram_solve(code, nv, _ptr(gp), _ptr(sp), sp.numel(), sweep, cfg.max_iter, thresh2,
+        _lib.check(lib.bak_gram_solve(code, nv, _ptr(gp), _ptr(sp), gp.numel() // nv, sweep, cfg.max_iter, thresh2,
                                       _ptr(cols), ncols, stride, _ptr(norms), _ptr(G), _ptr(a), _ptr(delta),
                                       _ptr(hist), _ptr(ctrl), _ptr(status), st), "bak_gram_solve")
 

@@ -247,11 +247,19 @@ __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p)
 // workspace layout (bytes): G | gpart | sqpart | delta | ctrl | G partials (split-K)
 static int64_t gram_nblk() { return 2 * static_cast<int64_t>(device_sms()); }
 
+// rows of gpart: the pass partials, or the fused first-sweep partials of the G kernel
+static int64_t gram_gpart_rows(int64_t obs, int64_t vars) {
+  int g0rows;
+  int64_t chunk;
+  gram_g_workspace(obs, vars, g0rows, chunk);
+  return g0rows > gram_nblk() ? g0rows : gram_nblk();
+}
+
 int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars) {
   (void)dtype;
   int64_t b = 0;
   b += vars * vars * 8;
-  b += gram_nblk() * vars * 8;
+  b += gram_gpart_rows(obs, vars) * vars * 8;
   b += gram_nblk() * 8;
   b += vars * 8;
   b += 64;
@@ -277,7 +285,7 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
   double* G = reinterpret_cast<double*>(w);
   w += vars * vars * 8;
   double* gpart = reinterpret_cast<double*>(w);
-  w += nblk * vars * 8;
+  w += gram_gpart_rows(prm.obs, vars) * vars * 8;
   double* sqpart = reinterpret_cast<double*>(w);
   w += nblk * 8;
   double* delta = reinterpret_cast<double*>(w);
@@ -288,7 +296,11 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
   const int64_t gparts_bytes = wsb - (reinterpret_cast<char*>(gparts_ws) - static_cast<char*>(ws));
 
   // ---- G = X^T X: hand-written fp64 DMMA SYRK (bak_gram_dmma.cu) ----
-  if (int rc = launch_gram_g(dtype, prm.x, prm.obs, prm.ldx, vars, G, gparts_ws, gparts_bytes, st)) return rc;
+  // G and the first sweep's g = X^T e (fused into the diagonal-block CTAs)
+  const bool fuse_g0 = reinterpret_cast<uintptr_t>(prm.e) % 16 == 0;
+  if (int rc = launch_gram_g(dtype, prm.x, prm.obs, prm.ldx, vars, G, gparts_ws, gparts_bytes, st, nullptr,
+                             fuse_g0 ? prm.e : nullptr, fuse_g0 ? gpart : nullptr))
+    return rc;
   BAK_CHECK_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(GramCtrl), st));
 
   PassParams pp{prm.x, prm.obs, prm.ldx, vars, prm.e, delta, 0, 1, gpart, sqpart, ctrl};
@@ -320,10 +332,19 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
     BAK_CHECK_CUDA(cudaGetLastError());
     return BAK_OK;
   };
-  int rc = pass(0, 1);
-  if (rc) return rc;
+  int rc = 0;
+  const int64_t pass_parts = sp.nblk;
+  if (fuse_g0) {
+    int g0rows;
+    int64_t chunk;
+    gram_g_workspace(prm.obs, vars, g0rows, chunk);
+    sp.nblk = g0rows;
+  } else if ((rc = pass(0, 1))) {
+    return rc;
+  }
   for (int64_t s = 1; s <= prm.max_iter; ++s) {
     if ((rc = solve(s))) return rc;
+    sp.nblk = pass_parts;
     if ((rc = pass(1, s < prm.max_iter ? 1 : 0))) return rc;
     if (prm.thresh2 >= 0.0 && s % 16 == 0) {
       // early break: stop enqueueing once the device has flagged convergence
@@ -367,6 +388,31 @@ extern "C" int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t va
     return BAK_EINVAL;
   }
   return launch_gram_g(dtype, x, obs, ldx, vars, G, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t bak_gram_dot_rows(int dtype, int64_t obs, int64_t vars) {
+  (void)dtype;
+  int nchunks;
+  int64_t chunk;
+  gram_g_workspace(obs, vars, nchunks, chunk);
+  return nchunks;
+}
+
+extern "C" int bak_gram_matrix_dot(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
+                                   const void* e, double* g0, void* workspace, int64_t workspace_bytes,
+                                   void* stream) {
+  if ((dtype != BAK_F32 && dtype != BAK_F64) || obs < 1 || vars < 1 || ldx < obs || !x || !G || !e || !g0) {
+    set_error("bak_gram_matrix_dot: bad arguments");
+    return BAK_EINVAL;
+  }
+  const size_t ts = dtype_size(dtype);
+  if (reinterpret_cast<uintptr_t>(x) % 16 || (ldx * static_cast<int64_t>(ts)) % 16 ||
+      reinterpret_cast<uintptr_t>(e) % 16) {
+    set_error("bak_gram_matrix_dot: x and e must be 16-byte aligned with ldx*sizeof(T) %% 16 == 0");
+    return BAK_EINVAL;
+  }
+  return launch_gram_g(dtype, x, obs, ldx, vars, G, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
+                       nullptr, e, g0);
 }
 
 extern "C" int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
@@ -458,7 +504,7 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
   double* G = reinterpret_cast<double*>(w);
   w += vars * vars * 8;
   double* gpart = reinterpret_cast<double*>(w);
-  w += nblk * vars * 8;
+  w += gram_gpart_rows(obs, vars) * vars * 8;
   double* sqpart = reinterpret_cast<double*>(w);
   w += nblk * 8;
   double* delta = reinterpret_cast<double*>(w);
@@ -468,7 +514,10 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
   double* gparts_ws = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
   const int64_t gparts_bytes = workspace_bytes - (reinterpret_cast<char*>(gparts_ws) - static_cast<char*>(workspace));
   BAK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int64_t), st));
-  if (int rc = launch_gram_g(dtype, x, obs, ldx, vars, G, gparts_ws, gparts_bytes, st, norms2_out)) return rc;
+  const bool fuse_g0 = reinterpret_cast<uintptr_t>(e) % 16 == 0;
+  if (int rc = launch_gram_g(dtype, x, obs, ldx, vars, G, gparts_ws, gparts_bytes, st, norms2_out,
+                             fuse_g0 ? e : nullptr, fuse_g0 ? gpart : nullptr))
+    return rc;
   // all-zero matrix -> the reference's ValueError (bak.py:186-187)
   {
     std::vector<unsigned char> h(static_cast<size_t>(vars) * ts);
@@ -513,10 +562,19 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
     BAK_CHECK_CUDA(cudaGetLastError());
     return BAK_OK;
   };
-  int rc = pass(0, 1, false);
-  if (rc) return rc;
+  int rc = 0;
+  const int64_t pass_parts = sp.nblk;
+  if (fuse_g0) {  // the first g came out of the G kernel
+    int g0rows;
+    int64_t chunk;
+    gram_g_workspace(obs, vars, g0rows, chunk);
+    sp.nblk = g0rows;
+  } else if ((rc = pass(0, 1, false))) {
+    return rc;
+  }
   for (int64_t s = 1; s <= max_iter; ++s) {
     if ((rc = solve(s))) return rc;
+    sp.nblk = pass_parts;
     if ((rc = pass(1, s < max_iter ? 1 : 0, s == max_iter))) return rc;
     if (thresh2 >= 0.0 && s % 16 == 0) {
       int64_t done = 0;

@@ -5,10 +5,15 @@
 // Only the lower block triangle of 64x64 blocks is computed (bi >= bj), split
 // over K (rows of x) into chunks; a CTA = 4 warps owns one (block, chunk) and
 // each warp a 32x32 quarter = 4x4 DMMA tiles.  Panels of 32 rows x 64 columns
-// stream through a 3-stage cp.async ring (zero-filled past obs / vars); panel
-// layout is column-major with a 36-element column stride so that the
-// m8n8k4 fragment loads (8 columns x 4 rows per warp) are bank-conflict free.
-// Partials per chunk are summed in chunk order (deterministic) and mirrored.
+// stream through a 2-stage cp.async ring (zero-filled past obs / vars), 3 CTAs
+// per SM in one wave; panel layout is column-major with a 36-element column
+// stride so that the m8n8k4 fragment loads (8 columns x 4 rows per warp) are
+// bank-conflict free.  Partials per chunk are summed in chunk order
+// (deterministic) and mirrored.  Diagonal-block CTAs optionally also produce
+// the first sweep's g = X^T e (warp 1, whose quarter of a diagonal block is
+// unused), so the solve skips its first pass over x.
+#include <cstdlib>
+
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
 
@@ -18,7 +23,6 @@ namespace {
 constexpr int kBT = 64;       // G block edge
 constexpr int kKT = 32;       // rows per panel stage
 constexpr int kLd = 36;       // smem column stride (elements)
-constexpr int kStages = 3;
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -40,36 +44,51 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 struct GramParams {
   const void* x;
   int64_t obs, ldx, vars;
-  int nb;            // number of 64-column blocks
-  int nchunks;       // K split
-  int64_t chunk;     // rows per chunk (multiple of kKT)
-  double* part;      // [nchunks][nblocks_lower][64*64]
+  int nb;                       // number of 64-column blocks
+  int cd, co;                   // K chunks per diagonal / off-diagonal block
+  int64_t chunk_d, chunk_o;     // rows per chunk (multiples of kKT)
+  double* part;                 // [nb*cd + noff*co][64*64], diagonal CTAs first
+  const void* e;                // optional: fused g0 = X^T e in the diagonal CTAs
+  double* g0;                   // [cd][vars] per-chunk partials of X^T e
 };
 
-// block index -> (bi, bj) with bi >= bj, row-major over the lower triangle
-__device__ __forceinline__ void tri_index(int b, int& bi, int& bj) {
-  bi = 0;
-  while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
-  bj = b - bi * (bi + 1) / 2;
+// off-diagonal block index -> (bi, bj), bi > bj, row-major over the strict lower triangle
+__device__ __forceinline__ void tri_index_strict(int o, int& bi, int& bj) {
+  bi = 1;
+  while ((bi + 1) * bi / 2 <= o) ++bi;
+  bj = o - bi * (bi - 1) / 2;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams p) {
+template <typename T, int kStages, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const GramParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* pa = reinterpret_cast<T*>(smem_raw);                  // [stages][64][kLd]
-  T* pb = pa + static_cast<size_t>(kStages) * kBT * kLd;  // [stages][64][kLd]
-  const int nblk = p.nb * (p.nb + 1) / 2;
-  const int blk = blockIdx.x % nblk;  // blocks of one chunk are adjacent: shared rows hit in L2
-  const int chk = blockIdx.x / nblk;
-  int bi, bj;
-  tri_index(blk, bi, bj);
-  const bool diag = bi == bj;
+  T* pb = pa + static_cast<size_t>(kStages) * kBT * kLd;  // [stages][64][kLd] (diagonal CTAs: e panel)
+  // Load balance: a diagonal block needs 3 of the 4 warp quarters, so its CTAs
+  // take 4/3 as many rows (cd ~ 3/4 co).  Diagonal CTAs come first.
+  const int ndc = p.nb * p.cd;
+  const bool diag = static_cast<int>(blockIdx.x) < ndc;
+  int bi, bj, chk;
+  int64_t chunk;
+  if (diag) {
+    bi = bj = blockIdx.x % p.nb;
+    chk = blockIdx.x / p.nb;
+    chunk = p.chunk_d;
+  } else {
+    const int noff = p.nb * (p.nb - 1) / 2;
+    const int c = blockIdx.x - ndc;
+    tri_index_strict(c % noff, bi, bj);
+    chk = c / noff;
+    chunk = p.chunk_o;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = (warp >> 1) * 32, wj = (warp & 1) * 32;  // warp's quarter of the block
   const T* __restrict__ x = static_cast<const T*>(p.x);
-  const int64_t k_begin = static_cast<int64_t>(chk) * p.chunk;
-  const int64_t k_end = imin64(p.obs, k_begin + p.chunk);
-  const int nsteps = static_cast<int>((k_end - k_begin + kKT - 1) / kKT);
+  const T* __restrict__ ev = static_cast<const T*>(p.e);
+  const bool with_e = diag && ev != nullptr;
+  const int64_t k_begin = static_cast<int64_t>(chk) * chunk;
+  const int64_t k_end = imin64(p.obs, k_begin + chunk);
+  const int nsteps = k_end > k_begin ? static_cast<int>((k_end - k_begin + kKT - 1) / kKT) : 0;
   constexpr int kPer = 16 / sizeof(T);               // elements per 16-byte piece
   constexpr int kPieces = kKT / kPer;                // pieces per column per stage
   constexpr int kCopies = kBT * kPieces / kThreads;  // per thread per panel
@@ -95,7 +114,15 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
         cp_async16(pb + (static_cast<size_t>(slot) * kBT + col) * kLd + piece * kPer, src, bytes);
       }
     }
+    if (with_e && tid < kPieces) {  // the residual rows of this stage (diagonal CTAs only)
+      const int64_t row = k0 + tid * kPer;
+      const int64_t rem = k_end - row;
+      const int bytes = rem > 0 ? static_cast<int>(imin64(rem, kPer) * sizeof(T)) : 0;
+      cp_async16(pb + static_cast<size_t>(slot) * kBT * kLd + tid * kPer, bytes ? ev + row : ev, bytes);
+    }
   };
+  // fused g0 (warp 1 of a diagonal CTA owns the unused upper quadrant: no DMMA work)
+  double g0a = 0.0, g0b = 0.0;
 
   double acc[4][4][2];
 #pragma unroll
@@ -135,9 +162,27 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
           for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
       }
     }
+    if (with_e && warp == 1) {
+      // columns lane and lane+32; rows in a lane-rotated order (conflict-free banks),
+      // fixed per column -> deterministic
+      const T* E = pb + static_cast<size_t>(slot) * kBT * kLd;
+#pragma unroll 8
+      for (int k = 0; k < kKT; ++k) {
+        const int kk = (k + lane) & (kKT - 1);
+        const double er = static_cast<double>(E[kk]);
+        g0a = __fma_rn(static_cast<double>(A[lane * kLd + kk]), er, g0a);
+        g0b = __fma_rn(static_cast<double>(A[(lane + 32) * kLd + kk]), er, g0b);
+      }
+    }
+  }
+  if (with_e && warp == 1) {
+    const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane;
+    double* g = p.g0 + static_cast<int64_t>(chk) * p.vars;
+    if (c0 < p.vars) g[c0] = g0a;
+    if (c0 + 32 < p.vars) g[c0 + 32] = g0b;
   }
   cp_async_wait<0>();
-  double* out = p.part + (static_cast<size_t>(chk) * nblk + blk) * kBT * kBT;
+  double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -148,22 +193,26 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
     }
 }
 
-// G (vars x vars, full, symmetric) = sum over chunks of the lower block partials
+// G (vars x vars, full, symmetric) = sum over K chunks of the lower block partials
 template <typename T>
-__global__ void gram_reduce_kernel(const double* __restrict__ part, int nchunks, int nb, int64_t V,
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int nb, int cd, int co, int64_t V,
                                    double* __restrict__ G, T* __restrict__ norms) {
-  const int nblk = nb * (nb + 1) / 2;
-  const int blk = blockIdx.y;
+  const int blk = blockIdx.y;  // lower triangle, row-major
   int bi = 0;
   while ((bi + 1) * (bi + 2) / 2 <= blk) ++bi;
   const int bj = blk - bi * (bi + 1) / 2;
+  const int noff = nb * (nb - 1) / 2;
+  const bool dg = bi == bj;
+  const int nch = dg ? cd : co;
+  const size_t first = dg ? static_cast<size_t>(bi) : static_cast<size_t>(nb) * cd + bi * (bi - 1) / 2 + bj;
+  const size_t stride = dg ? nb : noff;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kBT * kBT; e += gridDim.x * blockDim.x) {
     const int i = e / kBT, j = e % kBT;
     const int64_t gi = static_cast<int64_t>(bi) * kBT + i, gj = static_cast<int64_t>(bj) * kBT + j;
     if (gi >= V || gj >= V) continue;
-    if (bi == bj && j > i) continue;  // diagonal block: lower half (mirrored below)
+    if (dg && j > i) continue;  // diagonal block: lower half (mirrored below)
     double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += part[(static_cast<size_t>(c) * nblk + blk) * kBT * kBT + e];
+    for (int c = 0; c < nch; ++c) s += part[(first + c * stride) * kBT * kBT + e];
     G[gj * V + gi] = s;  // column-major (gi, gj)
     G[gi * V + gj] = s;  // mirror (gj, gi)
     if (norms && gi == gj) norms[gi] = static_cast<T>(s);  // n2_j = G_jj (fp64-accumulated)
@@ -172,21 +221,61 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nchunks,
 
 }  // namespace
 
+static inline int imax_host(int a, int b) { return a > b ? a : b; }
+
+struct GramSplit {
+  int nb, cd, co;
+  int64_t chunk_d, chunk_o;
+};
+
+// CTAs per SM of the G kernel: 3 (2-stage ring, <=170 registers) keeps the DMMA
+// pipe ~75% busy vs ~65% at 2 CTAs (3-stage ring); tuning aid BAK_GRAM_OCC=2
+static int gram_occ() {
+  const char* o = getenv("BAK_GRAM_OCC");
+  return (o && o[0] == '2') ? 2 : 3;
+}
+
+static GramSplit gram_split(int64_t obs, int64_t vars) {
+  GramSplit g{};
+  g.nb = static_cast<int>((vars + kBT - 1) / kBT);
+  const int noff = g.nb * (g.nb - 1) / 2;
+  // one wave: 2 CTAs per SM (smem-bound); a diagonal CTA does 3/4 of the MMA work
+  // of an off-diagonal one, so it gets 4/3 of the rows
+  const int slots = gram_occ() * device_sms();
+  // Equal chunks for every block by default (measured faster at 3 CTAs/SM: the
+  // scheduler mixes block types per SM); BAK_GRAM_BALANCE=1 gives diagonal
+  // blocks (3 of 4 warp quarters busy) 4/3 of the rows.
+  const char* bal = getenv("BAK_GRAM_BALANCE");
+  if (!(bal && bal[0] == '1')) {
+    g.cd = g.co = imax_host(1, slots / (g.nb * (g.nb + 1) / 2));
+  } else if (noff == 0) {
+    g.co = 1;
+    g.cd = slots;
+  } else {
+    g.co = static_cast<int>(slots / (noff + 0.75 * g.nb));
+    if (g.co < 1) g.co = 1;
+    g.cd = (3 * g.co) / 4;
+    if (g.cd < 1) g.cd = 1;
+  }
+  g.chunk_d = round_up((obs + g.cd - 1) / g.cd, kKT);
+  g.chunk_o = round_up((obs + g.co - 1) / g.co, kKT);
+  g.cd = static_cast<int>((obs + g.chunk_d - 1) / g.chunk_d);
+  g.co = static_cast<int>((obs + g.chunk_o - 1) / g.chunk_o);
+  if (g.cd < 1) g.cd = 1;
+  if (g.co < 1) g.co = 1;
+  return g;
+}
+
 int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk) {
-  const int nb = static_cast<int>((vars + kBT - 1) / kBT);
-  const int nblk = nb * (nb + 1) / 2;
-  // one wave: 2 CTAs per SM (smem-bound), every CTA one block x one K-range
-  const int slots = 2 * device_sms();
-  nchunks = slots / nblk;
-  if (nchunks < 1) nchunks = 1;
-  chunk = round_up((obs + nchunks - 1) / nchunks, kKT);
-  nchunks = static_cast<int>((obs + chunk - 1) / chunk);
-  if (nchunks < 1) nchunks = 1;
-  return static_cast<int64_t>(nchunks) * nblk * kBT * kBT * 8;
+  const GramSplit g = gram_split(obs, vars);
+  nchunks = g.cd;  // partial rows of the fused g0
+  chunk = g.chunk_d;
+  const int64_t ctas = static_cast<int64_t>(g.nb) * g.cd + static_cast<int64_t>(g.nb) * (g.nb - 1) / 2 * g.co;
+  return ctas * kBT * kBT * 8;
 }
 
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
-                  int64_t part_bytes, cudaStream_t st, void* norms_out) {
+                  int64_t part_bytes, cudaStream_t st, void* norms_out, const void* e, double* g0) {
   int nchunks;
   int64_t chunk;
   const int64_t need = gram_g_workspace(obs, vars, nchunks, chunk);
@@ -194,29 +283,33 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
     set_error("gram: partial workspace too small");
     return BAK_EWORKSPACE;
   }
-  const int nb = static_cast<int>((vars + kBT - 1) / kBT);
-  const int nblk = nb * (nb + 1) / 2;
-  GramParams p{x, obs, ldx, vars, nb, nchunks, chunk, static_cast<double*>(part_ws)};
+  const GramSplit g = gram_split(obs, vars);
+  const int nblk = g.nb * (g.nb + 1) / 2;
+  GramParams p{x, obs, ldx, vars, g.nb, g.cd, g.co, g.chunk_d, g.chunk_o, static_cast<double*>(part_ws),
+               g0 ? e : nullptr, g0};
   const size_t ts = dtype == BAK_F64 ? 8 : 4;
-  const size_t smem = 2ull * kStages * kBT * kLd * ts;
-  const unsigned grid = static_cast<unsigned>(nchunks * nblk);
-  if (dtype == BAK_F64) {
-    BAK_CHECK_CUDA(cudaFuncSetAttribute(gram_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-    gram_dmma_kernel<double><<<grid, kThreads, smem, st>>>(p);
-  } else {
-    BAK_CHECK_CUDA(cudaFuncSetAttribute(gram_dmma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-    gram_dmma_kernel<float><<<grid, kThreads, smem, st>>>(p);
-  }
+  const unsigned grid = static_cast<unsigned>(g.nb * g.cd + g.nb * (g.nb - 1) / 2 * g.co);
+  auto go = [&](auto kern, int stages) -> int {
+    const size_t smem = 2ull * stages * kBT * kLd * ts;
+    BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, st>>>(p);
+    return BAK_OK;
+  };
+  const bool occ3 = gram_occ() == 3;
+  int rc;
+  if (dtype == BAK_F64)
+    rc = occ3 ? go(gram_dmma_kernel<double, 2, 3>, 2) : go(gram_dmma_kernel<double, 3, 2>, 3);
+  else
+    rc = occ3 ? go(gram_dmma_kernel<float, 2, 3>, 2) : go(gram_dmma_kernel<float, 3, 2>, 3);
+  if (rc) return rc;
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
   if (dtype == BAK_F64)
-    gram_reduce_kernel<double><<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), nchunks, nb, vars,
-                                                               G, static_cast<double*>(norms_out));
+    gram_reduce_kernel<double><<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), g.nb, g.cd, g.co,
+                                                               vars, G, static_cast<double*>(norms_out));
   else
-    gram_reduce_kernel<float><<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), nchunks, nb, vars,
-                                                              G, static_cast<float*>(norms_out));
+    gram_reduce_kernel<float><<<dim3(16, nblk), 256, 0, st>>>(static_cast<const double*>(part_ws), g.nb, g.cd, g.co,
+                                                              vars, G, static_cast<float*>(norms_out));
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
   return BAK_OK;

@@ -56,7 +56,8 @@ int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars);
 bool gram_supported(int64_t vars);
 int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk);
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
-                  int64_t part_bytes, cudaStream_t st, void* norms_out = nullptr);
+                  int64_t part_bytes, cudaStream_t st, void* norms_out = nullptr, const void* e = nullptr,
+                  double* g0 = nullptr);
 bool gram_tma_supported(int64_t vars);
 int gram_tma_grid(int dtype);
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,

@@ -45,6 +45,8 @@ extern "C" {
 #define BAK_ETIMEOUT     3 /* device-side spin wait exceeded its deadline */
 #define BAK_EUNSUPPORTED 4 /* shape/variant combination not supported     */
 #define BAK_EWORKSPACE   5 /* workspace too small                         */
+#define BAK_EDIVERGED    6 /* device status only: the blocked sweep's divergence
+                              guard tripped (bakp.py:121-124)             */
 
 /* Thread-local text of the last error ("" if none). */
 const char* bak_last_error(void);
@@ -188,6 +190,36 @@ int bak_copy_rows_h2d(void* dst, int64_t dld, const void* src, int64_t sld, int6
 int bak_ipc_get_handle(void* devptr, void* handle64);
 int bak_ipc_open_handle(const void* handle64, void** devptr);
 int bak_ipc_close(void* devptr);
+
+/* ---- blocked sweep: solve_bakp / block_deltas (bakp.py:52-185) -------------
+ * Replaces baksolve.bakp._run_block_sweeps (bakp.py:95-129), cyclic order:
+ * consecutive blocks of thr columns (narrower last block); per block every
+ * delta d_k = <x_k, e>/n2_k against the same stale e (0 for zero-norm
+ * columns), a[j0:j1] += d, e -= x_B d (T rounding of the product, then of the
+ * subtraction).  Per sweep: history[s] = sum(e^2); divergence guard (not
+ * finite, or > 10x the previous sum; the first reference is prev_sq = ||y||^2)
+ * -> status[2] = BAK_EDIVERGED with status[0] counting the diverged sweep;
+ * early break on thresh2 (< 0 disables).
+ *   variant : AUTO, CTA / CLUSTER (e on chip), STREAM (e in HBM, any shape),
+ *             GRAM (labelled algebraically-equivalent block substitution,
+ *             vars <= 512).
+ *   history : required, double[max_iter] (the guard message needs it).
+ *   status  : int64[4] device {sweeps_run, converged, error, variant_used}. */
+int bak_block_pick_variant(int dtype, int64_t obs, int64_t vars, int64_t thr);
+int64_t bak_block_sweep_workspace(int dtype, int variant, int64_t obs, int64_t vars, int64_t thr);
+int bak_block_sweep(int dtype, int variant,
+                    const void* x, int64_t obs, int64_t vars, int64_t ldx,
+                    const void* norms2, int64_t thr,
+                    void* e, void* a,
+                    int64_t max_iter, double thresh2, double prev_sq,
+                    double* history, int64_t* status,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+/* block_deltas (bakp.py:65-85): out[k - j0] = <x_k, e>/n2_k for k in [j0, j1),
+ * 0 where n2_k == 0; 0 <= j0 < j1 <= vars. */
+int64_t bak_block_deltas_workspace(int dtype, int64_t obs);
+int bak_block_deltas(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx,
+                     int64_t j0, int64_t j1, const void* e, const void* norms2, void* out,
+                     void* workspace, int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

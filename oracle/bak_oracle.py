@@ -28,6 +28,8 @@ Reference map (``/root/reference/pkg/src/baksolve``):
   finish / drift     bak.py:127-143 (_finish_report), DRIFT_TOL bak.py:29
   solve              bak.py:146-195 (solve_bak)
   fp64 metrics       bench.py:109-121 (_predict_f64), bench.py:180-184
+  blocked solver     bakp.py:52-185 (block_deltas, _run_block_sweeps, solve_bakp),
+                     DIVERGENCE_FACTOR bakp.py:32
 """
 
 from __future__ import annotations
@@ -38,6 +40,11 @@ import numpy as np
 from threadpoolctl import threadpool_limits
 
 DRIFT_TOL = 1e-4                       # bak.py:29
+DIVERGENCE_FACTOR = 10.0               # bakp.py:32
+
+
+class DivergenceError(RuntimeError):
+    """bakp.py:35-36"""
 _DTYPES = {"single": np.float32, "double": np.float64}
 
 
@@ -202,6 +209,92 @@ def coordinate_update(col, e):
     np.multiply(col, step, out=tmp)
     np.subtract(e, tmp, out=tmp)
     return float(step), tmp
+
+
+def block_deltas(x, j0, j1, e, n2):
+    """Deltas of columns [j0, j1) against one stale residual (bakp.py:52-62):
+    one ?dot per column, T division, 0 for zero-norm columns."""
+    out = np.empty(j1 - j0, dtype=e.dtype)
+    for k in range(j0, j1):
+        out[k - j0] = 0.0 if n2[k] == 0.0 else np.dot(x[:, k], e) / n2[k]
+    return out
+
+
+def block_sweep_loop(x, e, a, n2, tmp, thr, max_iter, thresh2, history, prev_sq):
+    """bakp.py:95-129: consecutive blocks of thr columns (narrower last block);
+    a one-column block is the sequential column step (bakp.py:102-106), a wider
+    block gets its deltas against the stale e, then a[j0:j1] += d and
+    e -= x_B @ d (?gemv into scratch, then one subtraction, bakp.py:114-116).
+    The divergence guard (bakp.py:121-124) and early break run once per sweep."""
+    nvars = x.shape[1]
+    sweeps = 0
+    for _ in range(max_iter):
+        for j0 in range(0, nvars, thr):
+            j1 = min(j0 + thr, nvars)
+            if j1 - j0 == 1:
+                nj = n2[j0]
+                if nj != 0.0:
+                    xj = x[:, j0]
+                    step = np.dot(xj, e) / nj
+                    np.multiply(xj, step, out=tmp)
+                    np.subtract(e, tmp, out=e)
+                    a[j0] += step
+                continue
+            dv = block_deltas(x, j0, j1, e, n2)
+            a[j0:j1] += dv
+            np.matmul(x[:, j0:j1], dv, out=tmp)
+            np.subtract(e, tmp, out=e)
+        sweeps += 1
+        sq = float(np.dot(e, e))
+        if history is not None:
+            history.append(sq)
+        if not np.isfinite(sq) or sq > prev_sq * DIVERGENCE_FACTOR:
+            raise DivergenceError(
+                f"residual norm grew from {prev_sq:.6g} to {sq:.6g} in one sweep "
+                f"with thr={thr}; use a smaller thr")
+        prev_sq = sq
+        if thresh2 is not None and sq <= thresh2:
+            return sweeps, True
+    return sweeps, False
+
+
+def solve_bakp(x, y, max_iter=1000, tol=1e-6, thr=1, record_history=False):
+    """Restatement of ``solve_bakp`` (bakp.py:132-185), cyclic order only.
+    Worker threads of the reference do not change its bits (bakp.py:10-15), so
+    this is single-threaded."""
+    if thr < 1:
+        raise ValueError(f"thr must be >= 1, got {thr}")
+    x = _coerce_matrix(x)
+    obs, nvars = x.shape
+    if thr > nvars:
+        raise ValueError(f"thr={thr} exceeds the number of columns ({nvars})")
+    y = _coerce_vector(y, x.dtype)
+    if y.shape[0] != obs:
+        raise ValueError(f"y has length {y.shape[0]}, expected {obs}")
+    t0 = time.perf_counter()
+    ynorm2 = float(np.dot(y, y))
+    if ynorm2 == 0.0:
+        return dict(a_hat=np.zeros(nvars, x.dtype), residual=np.zeros(obs, x.dtype),
+                    residual_norm_history=[] if record_history else None,
+                    sweeps_run=0, converged=True, wall_time=time.perf_counter() - t0,
+                    drift_warning=False, e=np.zeros(obs, x.dtype))
+    history = [] if record_history else None
+    thresh2 = tol * tol * ynorm2 if tol > 0 else None
+    a = np.zeros(nvars, dtype=x.dtype)
+    with threadpool_limits(limits=1, user_api="blas"):
+        n2 = column_norms_sq(x)
+        if not n2.any():
+            raise ValueError("every column of x has zero norm; nothing to solve")
+        e = y.copy()
+        tmp = np.empty_like(e)
+        sweeps, converged = block_sweep_loop(x, e, a, n2, tmp, thr, max_iter, thresh2, history, ynorm2)
+        resid = y - x @ a
+        wall = time.perf_counter() - t0
+        drift = np.linalg.norm((e - resid).astype(np.float64))
+        drift_rel = drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny)
+    return dict(a_hat=a, residual=resid, residual_norm_history=history,
+                sweeps_run=sweeps, converged=converged, wall_time=wall,
+                drift_warning=bool(drift_rel > DRIFT_TOL), e=e)
 
 
 def permutations(ordering_seed, nvars, nsweeps):

@@ -6,15 +6,19 @@ the reference package ``baksolve`` 0.1.0 (arXiv 2104.12570, Algorithm 1).
 
 Names mirror ``baksolve`` (reference __init__.py:9-10): SolveConfig,
 SolveReport, solve_bak, coordinate_update, residual_norm, DRIFT_TOL.
+The blocked solver of the reference's bakp.py (Algorithm 2): solve_bakp,
+block_deltas, BlockConfig, DivergenceError, DIVERGENCE_FACTOR.
 Extension: solve_bak_batched for many independent small systems.
 """
 
 from .bak import (DRIFT_TOL, ORDERINGS, BatchSolveReport, DeviceBatch, DeviceMatrix, SolveConfig, SolveReport,
                   colnorms, coordinate_update, residual_norm, solve_bak, solve_bak_batched, to_device_batch,
                   to_device_matrix)
+from .bakp import DIVERGENCE_FACTOR, BlockConfig, DivergenceError, block_deltas, solve_bakp
 
 __version__ = "0.1.0"
 
-__all__ = ["DRIFT_TOL", "ORDERINGS", "BatchSolveReport", "DeviceBatch", "DeviceMatrix", "SolveConfig",
-           "SolveReport", "colnorms", "coordinate_update", "residual_norm", "solve_bak", "solve_bak_batched",
-           "to_device_batch", "to_device_matrix"]
+__all__ = ["DIVERGENCE_FACTOR", "DRIFT_TOL", "ORDERINGS", "BatchSolveReport", "BlockConfig", "DeviceBatch",
+           "DeviceMatrix", "DivergenceError", "SolveConfig", "SolveReport", "block_deltas", "colnorms",
+           "coordinate_update", "residual_norm", "solve_bak", "solve_bak_batched", "solve_bakp", "to_device_batch",
+           "to_device_matrix"]

@@ -13,6 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbak200.so")
 
 F32, F64 = 0, 1
+EDIVERGED = 6  # device status: the blocked sweep's divergence guard tripped
 VARIANTS = {"auto": 0, "cta": 1, "cluster": 2, "grid": 3, "stream": 4, "gram": 5}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
@@ -42,6 +43,12 @@ SIGNATURES = {
     "bak_gram_matrix_workspace": (_i64, [_int, _i64, _i64]),
     "bak_gram_matrix": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
     "bak_gram_dot_rows": (_i64, [_int, _i64, _i64]),
+    "bak_block_pick_variant": (_int, [_int, _i64, _i64, _i64]),
+    "bak_block_sweep_workspace": (_i64, [_int, _int, _i64, _i64, _i64]),
+    "bak_block_sweep": (_int, [_int, _int, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp,
+                               _vp, _i64, _vp]),
+    "bak_block_deltas_workspace": (_i64, [_int, _i64]),
+    "bak_block_deltas": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_matrix_dot": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
     "bak_gram_pass_resid": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,

@@ -165,7 +165,14 @@ struct SolveParams {
   double* history;
   GramCtrl* ctrl;
   int64_t* status;
+  int64_t thr = 1;     // > 1: blocked sweep (bakp.py:95-129), cyclic order only
+  int guard = 0;       // divergence guard of the blocked sweep (bakp.py:121-124)
+  double prev0 = 0.0;  // the guard's first reference value, ||y||^2
 };
+
+__device__ __forceinline__ bool gram_diverged(double sq, double prev) {
+  return !(sq <= 1.79769313486231570815e308 && sq >= -1.79769313486231570815e308) || sq > prev * 10.0;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p) {
@@ -184,22 +191,30 @@ __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p)
     __syncthreads();
     double sq = 0.0;
     for (int w = 0; w < static_cast<int>(blockDim.x) / 32; ++w) sq += wsum[w];
-    const bool stop_conv = p.thresh2 >= 0.0 && sq <= p.thresh2;
+    bool stop_div = false;
+    if (p.guard) {
+      const double prev = (s == 2) ? p.prev0 : __longlong_as_double(p.ctrl->pad);
+      stop_div = gram_diverged(sq, prev);
+      __syncthreads();  // every thread has read prev before it is replaced
+    }
+    const bool stop_conv = !stop_div && p.thresh2 >= 0.0 && sq <= p.thresh2;
     const bool stop_max = (s - 1) >= p.max_iter;
     if (tid == 0) {
       if (p.history) p.history[s - 2] = sq;
-      if (stop_conv || stop_max) {
+      if (p.guard) p.ctrl->pad = __double_as_longlong(sq);
+      if (stop_conv || stop_max || stop_div) {
         p.ctrl->done = 1;
         p.ctrl->sweeps = s - 1;
         p.ctrl->converged = stop_conv ? 1 : 0;
         if (p.status) {
           p.status[0] = s - 1;
           p.status[1] = stop_conv ? 1 : 0;
+          if (stop_div) p.status[2] = BAK_EDIVERGED;
           p.status[3] = BAK_VARIANT_GRAM;
         }
       }
     }
-    if (stop_conv || stop_max) return;
+    if (stop_conv || stop_max || stop_div) return;
   }
   // g = sum over pass CTAs (fixed order), residual dots in double
   __shared__ int ord[512];
@@ -217,6 +232,28 @@ __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p)
   }
   double dj = 0.0;
   __syncthreads();
+  if (p.thr > 1) {
+    // blocked sweep: every delta of a block from the same (stale) residual dots,
+    // then one correction of the dots by the block (bakp.py:101-116)
+    __shared__ double dblk[512];
+    for (int64_t j0 = 0; j0 < p.ncols; j0 += p.thr) {
+      const int64_t j1 = imin64(j0 + p.thr, p.ncols);
+      if (tid >= j0 && tid < j1) {
+        const T d = (n2s[tid] != 0.0) ? Num<T>::div(static_cast<T>(rj), static_cast<T>(n2s[tid])) : T(0);
+        dblk[tid] = static_cast<double>(d);
+        dj = static_cast<double>(d);
+        aj = Num<T>::add(aj, d);
+      }
+      __syncthreads();
+      if (tid < V)
+        for (int64_t k = j0; k < j1; ++k) rj = __fma_rn(-p.G[k * V + tid], dblk[k], rj);
+    }
+    if (tid < V) {
+      p.delta[tid] = dj;
+      a[tid] = aj;
+    }
+    return;
+  }
   // forward substitution over the sweep order; G column of the next step prefetched
   double gnext = (tid < V && p.ncols > 0) ? p.G[static_cast<int64_t>(ord[0]) * V + tid] : 0.0;
   for (int64_t kk = 0; kk < p.ncols; ++kk) {
@@ -271,7 +308,40 @@ int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars) {
 
 bool gram_supported(int64_t vars) { return vars >= 1 && vars <= 512; }
 
+static int launch_gram_impl(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st,
+                            int64_t thr, int guard, double prev0);
+
 int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st) {
+  return launch_gram_impl(dtype, prm, vars, ws, wsb, st, 1, 0, 0.0);
+}
+
+int launch_gram_block(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, const void* norms2,
+                      int64_t thr, void* e, void* a, int64_t max_iter, double thresh2, double prev_sq,
+                      double* history, int64_t* status, void* ws, int64_t wsb, cudaStream_t st) {
+  if (reinterpret_cast<uintptr_t>(e) % 16) {
+    set_error("bak_block_sweep(GRAM): e must be 16-byte aligned");
+    return BAK_EINVAL;
+  }
+  SweepParams prm{};
+  prm.x = x;
+  prm.obs = obs;
+  prm.ldx = ldx;
+  prm.norms2 = norms2;
+  prm.cols = nullptr;
+  prm.ncols = vars;
+  prm.cols_stride = 0;
+  prm.e = e;
+  prm.a = a;
+  prm.max_iter = max_iter;
+  prm.thresh2 = thresh2;
+  prm.history = history;
+  prm.status = status;
+  BAK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int64_t), st));
+  return launch_gram_impl(dtype, prm, vars, ws, wsb, st, thr, 1, prev_sq);
+}
+
+static int launch_gram_impl(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st,
+                            int64_t thr, int guard, double prev0) {
   if (!gram_supported(vars)) {
     set_error("GRAM variant supports 1 <= vars <= 512 (got %lld)", (long long)vars);
     return BAK_EUNSUPPORTED;
@@ -305,7 +375,7 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
 
   PassParams pp{prm.x, prm.obs, prm.ldx, vars, prm.e, delta, 0, 1, gpart, sqpart, ctrl};
   SolveParams sp{vars, nblk, 0, prm.max_iter, prm.thresh2, prm.cols, prm.ncols, prm.cols_stride, prm.norms2,
-                 G, gpart, sqpart, prm.a, delta, prm.history, ctrl, prm.status};
+                 G, gpart, sqpart, prm.a, delta, prm.history, ctrl, prm.status, thr, guard, prev0};
   const bool use_tma = gram_tma_supported(vars);
   if (use_tma) sp.nblk = gram_tma_grid(dtype);
   auto pass = [&](int apply, int dot) -> int {
@@ -346,8 +416,8 @@ int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64
     if ((rc = solve(s))) return rc;
     sp.nblk = pass_parts;
     if ((rc = pass(1, s < prm.max_iter ? 1 : 0))) return rc;
-    if (prm.thresh2 >= 0.0 && s % 16 == 0) {
-      // early break: stop enqueueing once the device has flagged convergence
+    if ((prm.thresh2 >= 0.0 || guard) && s % 16 == 0) {
+      // early break: stop enqueueing once the device has flagged convergence (or divergence)
       int64_t done = 0;
       BAK_CHECK_CUDA(cudaMemcpyAsync(&done, &ctrl->done, sizeof(done), cudaMemcpyDeviceToHost, st));
       BAK_CHECK_CUDA(cudaStreamSynchronize(st));

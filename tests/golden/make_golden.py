@@ -3,6 +3,7 @@
 Run in the build container, where the reference is mounted read-only:
 
     python tests/golden/make_golden.py            # writes tests/golden/*.npz
+    python tests/golden/make_golden.py --bakp-only   # only the bakp_*.npz fixtures
 
 The reference is imported from ``/root/reference/pkg/src`` (pure Python on
 numpy/OpenBLAS).  Nothing at test time reads ``/root/reference``: the
@@ -47,6 +48,14 @@ def main():
     host = {"numpy": np.__version__,
             "blas": (blas[0].get("internal_api"), blas[0].get("version"),
                      blas[0].get("architecture")) if blas else None}
+
+    if "--bakp-only" in sys.argv:  # regenerate only the blocked-solver fixtures
+        with open(os.path.join(HERE, "MANIFEST.json")) as f:
+            man = json.load(f)
+        man["bakp_cases"] = make_bakp(bk, host, _predict_f64)
+        with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
+            json.dump(man, f, indent=1)
+        return
 
     cases = []
 
@@ -153,8 +162,105 @@ def main():
     da, e_next = bk.coordinate_update(np.array([1.0, 2.0]), np.array([3.0, 4.0]))
     np.savez_compressed(os.path.join(HERE, "kat_coordinate_update.npz"),
                         col=np.array([1.0, 2.0]), e=np.array([3.0, 4.0]), da=np.array(da), e_next=e_next)
+    bakp_cases = make_bakp(bk, host, _predict_f64)
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
-        json.dump({"host": host, "cases": cases, "reference": "baksolve 0.1.0 (/root/reference/pkg)"}, f, indent=1)
+        json.dump({"host": host, "cases": cases, "bakp_cases": bakp_cases,
+                   "reference": "baksolve 0.1.0 (/root/reference/pkg)"}, f, indent=1)
+
+
+def make_bakp(bk, host, _predict_f64):
+    """Fixtures of the blocked solver (bakp.py:132-185), files bakp_*.npz.
+    A case whose reference solve raises DivergenceError stores the message."""
+    cases = []
+
+    def add(name, x, y, cfg, thr, spec=None, store_inputs=True):
+        d = dict(thr=np.array(thr), max_iter=np.array(cfg.max_iter), tol=np.array(cfg.tol),
+                 record_history=np.array(cfg.record_history), dtype=np.array(np.dtype(x.dtype).name),
+                 shape=np.array(x.shape), host=np.array(json.dumps(host)),
+                 spec=np.array(json.dumps(spec) if spec else ""),
+                 input_sha=np.array(_sha(np.asfortranarray(x), y)))
+        try:
+            with np.errstate(invalid="ignore", over="ignore"):
+                rep = bk.solve_bakp(x, y, bk.BlockConfig(base=cfg, thr=thr, worker_count=1))
+        except bk.DivergenceError as err:
+            d.update(diverged=np.array(True), message=np.array(str(err)))
+            info = f"DivergenceError: {err}"
+        else:
+            pred = _predict_f64(x, rep.a_hat)
+            d.update(diverged=np.array(False), a_hat=rep.a_hat, residual=rep.residual,
+                     history=np.asarray(rep.residual_norm_history or [], np.float64),
+                     has_history=np.array(rep.residual_norm_history is not None),
+                     sweeps_run=np.array(rep.sweeps_run), converged=np.array(rep.converged),
+                     drift_warning=np.array(rep.drift_warning),
+                     resid_norm_f64=np.array(float(np.linalg.norm(np.asarray(y, np.float64) - pred))),
+                     ynorm_f64=np.array(float(np.linalg.norm(np.asarray(y, np.float64)))))
+            info = f"sweeps={rep.sweeps_run} conv={rep.converged}"
+        if store_inputs:
+            d["x"] = np.asfortranarray(x)
+            d["y"] = np.asarray(y)
+        np.savez_compressed(os.path.join(HERE, f"bakp_{name}.npz"), **d)
+        cases.append("bakp_" + name)
+        print(f"bakp_{name:24s} {str(x.shape):>14s} {x.dtype} thr={thr} {info}")
+
+    SC = bk.SolveConfig
+
+    def consistent(rng, obs, nv, dtype, noise=0.0):
+        x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+        y = (x @ rng.uniform(-1, 1, nv).astype(dtype)).astype(dtype)
+        if noise:
+            y = (y + noise * rng.standard_normal(obs)).astype(dtype)
+        return x, y
+
+    rng = np.random.default_rng(2)
+    x, y = consistent(rng, 120, 17, np.float64, 0.1)
+    add("thr1_120x17_f64", x, y, SC(max_iter=30, tol=1e-7, record_history=True), 1)
+    x, y = consistent(rng, 90, 8, np.float32, 0.1)
+    add("thr1_90x8_f32", x, y, SC(max_iter=30, tol=1e-7, record_history=True), 1)
+    rng = np.random.default_rng(3)
+    x, y = consistent(rng, 250, 48, np.float32, 0.05)
+    add("thr16_250x48_f32", x, y, SC(max_iter=25, tol=1e-6, record_history=True), 16)
+    rng = np.random.default_rng(6)
+    x = np.asfortranarray(rng.standard_normal((35, 10)))
+    add("thr4_35x10_f64", x, rng.standard_normal(35), SC(max_iter=3, tol=0, record_history=True), 4)
+    rng = np.random.default_rng(5)
+    x = np.asfortranarray(rng.standard_normal((40, 7)))
+    add("thr3_remainder_40x7_f64", x, x @ np.ones(7), SC(max_iter=1, tol=0), 3)
+    rng = np.random.default_rng(4)
+    q, _ = np.linalg.qr(rng.standard_normal((60, 8)))
+    add("orthonormal_full_60x8_f64", np.asfortranarray(q), rng.standard_normal(60), SC(max_iter=1, tol=0), 8)
+    rng = np.random.default_rng(200)
+    x, y = consistent(rng, 300, 100, np.float64)
+    add("thr10_300x100_f64", x, y, SC(max_iter=60, tol=1e-8, record_history=True), 10)
+    rng = np.random.default_rng(31)
+    x, y = consistent(rng, 400, 60, np.float32, 0.1)
+    add("thr6_400x60_f32", x, y, SC(max_iter=600, tol=0), 6)
+    rng = np.random.default_rng(41)
+    x = np.asfortranarray(rng.standard_normal((50, 8)))
+    x[:, 2] = 0.0
+    x[:, 5] = 0.0
+    add("zero_columns_50x8_f64", x, rng.standard_normal(50), SC(max_iter=40, tol=0, record_history=True), 4)
+    rng = np.random.default_rng(42)
+    x = np.asfortranarray(rng.standard_normal((2000, 40)))
+    add("thr7_2000x40_f64", x, rng.standard_normal(2000), SC(max_iter=50, tol=0, record_history=True), 7)
+    rng = np.random.default_rng(43)
+    x = np.asfortranarray(rng.standard_normal((40, 100)))
+    add("wide_thr10_40x100_f64", x, x @ rng.standard_normal(100), SC(max_iter=50, tol=1e-6, record_history=True), 10)
+    rng = np.random.default_rng(21)
+    col = rng.standard_normal(50)
+    add("diverge_dup_50x5_f64", np.asfortranarray(np.tile(col[:, None], (1, 5))), col.copy(), SC(max_iter=10), 5)
+    add("diverge_nan_2x1_f32", np.asfortranarray(np.array([[1e30], [0.0]], dtype=np.float32)),
+        np.array([1e30, 0.0], dtype=np.float32), SC(max_iter=5), 1)
+    spec = dict(obs=10000, vars=1000, seed=6, distribution="uniform", coeff_distribution="uniform",
+                noise_sigma=0.0, precision="single")
+    x, y, _ = bk.generate_system(bk.SystemSpec(obs=10000, vars=1000, seed=6), "single")
+    add("paper_10000x1000_f32_thr50", x, y, SC(max_iter=200, tol=1e-6, record_history=True), 50, spec=spec,
+        store_inputs=False)
+    # block_deltas KATs (test_solver_bakp.py:18-34)
+    np.savez_compressed(os.path.join(HERE, "kat_block_deltas.npz"),
+                        eye=bk.block_deltas(np.eye(2, order="F"), (0, 2), np.array([3.0, 4.0])),
+                        dup=bk.block_deltas(np.asfortranarray(np.column_stack([[1.0, 2.0, -1.0]] * 2)), (0, 2),
+                                            np.array([1.0, 2.0, -1.0])))
+    return cases
 
 
 if __name__ == "__main__":

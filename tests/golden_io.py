@@ -12,7 +12,29 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith("kat_coordinate"))
+                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_")))
+
+
+def bakp_names():
+    """Fixtures of the blocked solver (bakp.py), made by make_golden.make_bakp."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "bakp_*.npz")))
+
+
+def load_bakp(name):
+    with np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    spec = str(d["spec"])
+    if "x" not in d:
+        from oracle import bak_oracle as orc
+        s = json.loads(spec)
+        x, y, _ = orc.make_system(s["obs"], s["vars"], s["seed"], s["distribution"],
+                                  s["coeff_distribution"], s["noise_sigma"], s["precision"])
+        d["x"], d["y"] = x, y
+    d["config"] = dict(max_iter=int(d["max_iter"]), tol=float(d["tol"]), record_history=bool(d["record_history"]))
+    d["thr"] = int(d["thr"])
+    d["diverged"] = bool(d["diverged"])
+    d["host"] = json.loads(str(d["host"]))
+    return d
 
 
 def load(name):

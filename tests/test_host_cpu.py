@@ -95,3 +95,23 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh")):
                 with open(os.path.join(dirpath, f)) as fh:
                     assert "oracle" not in fh.read().replace("oracle/", ""), f
+
+
+def test_block_config_validation_cpu():
+    """BlockConfig mirrors bakp.py:39-49 (pure host logic)."""
+    from paper_2104_12570_b200 import BlockConfig, SolveConfig
+    assert BlockConfig().thr == 1 and BlockConfig().worker_count == 0
+    assert isinstance(BlockConfig().base, SolveConfig)
+    with pytest.raises(ValueError):
+        BlockConfig(thr=0)
+    with pytest.raises(ValueError):
+        BlockConfig(worker_count=-1)
+
+
+def test_divergence_first_sweep_logic_cpu():
+    from paper_2104_12570_b200.bakp import _divergence_message, _first_divergence
+    assert _first_divergence([5.0, 4.0, 3.0], 10.0) is None
+    assert _first_divergence([5.0, 60.0, 3.0], 10.0) == (5.0, 60.0)
+    assert _first_divergence([float("nan")], float("inf"))[0] == float("inf")
+    assert _divergence_message(44.9682, 719.49, 5) == (
+        "residual norm grew from 44.9682 to 719.49 in one sweep with thr=5; use a smaller thr")

@@ -78,3 +78,49 @@ def test_manifest_lists_every_fixture():
     with open(golden_io.os.path.join(golden_io.GOLDEN, "MANIFEST.json")) as f:
         man = json.load(f)
     assert sorted(man["cases"]) == golden_io.names()
+    assert sorted(man["bakp_cases"]) == golden_io.bakp_names()
+
+
+@pytest.mark.parametrize("name", golden_io.bakp_names())
+def test_oracle_bakp_matches_reference_fixture(name):
+    """solve_bakp restatement (bakp.py:132-185) against the reference's own runs."""
+    g = golden_io.load_bakp(name)
+    x, y = g["x"], g["y"]
+    assert golden_io.input_sha(x, y) == str(g["input_sha"])
+    if g["diverged"]:
+        with np.errstate(invalid="ignore", over="ignore"):
+            with pytest.raises(orc.DivergenceError) as ei:
+                orc.solve_bakp(x, y, thr=g["thr"], **g["config"])
+        if _same_blas(g["host"]):
+            assert str(ei.value) == str(g["message"])
+        return
+    out = orc.solve_bakp(x, y, thr=g["thr"], **g["config"])
+    assert out["sweeps_run"] == int(g["sweeps_run"])
+    assert out["converged"] == bool(g["converged"])
+    assert out["drift_warning"] == bool(g["drift_warning"])
+    if _same_blas(g["host"]):
+        assert out["a_hat"].tobytes() == g["a_hat"].tobytes()
+        assert out["residual"].tobytes() == g["residual"].tobytes()
+        if bool(g["has_history"]):
+            assert np.array_equal(np.asarray(out["residual_norm_history"]), g["history"])
+    else:
+        tol = 1e-10 if x.dtype == np.float64 else 1e-4
+        assert orc.rel_coeff_err(out["a_hat"], g["a_hat"]) <= tol
+
+
+def test_oracle_bakp_thr1_is_the_sweep():
+    """bakp.py:13-15: thr=1 reproduces solve_bak bit for bit."""
+    g = golden_io.load("c1_scaled_2000x40_f64")
+    a = orc.solve(g["x"], g["y"], max_iter=20, tol=0, record_history=True)
+    b = orc.solve_bakp(g["x"], g["y"], max_iter=20, tol=0, thr=1, record_history=True)
+    assert a["a_hat"].tobytes() == b["a_hat"].tobytes()
+    assert a["residual_norm_history"] == b["residual_norm_history"]
+
+
+def test_block_deltas_kat():
+    with np.load(golden_io.os.path.join(golden_io.GOLDEN, "kat_block_deltas.npz")) as z:
+        np.testing.assert_array_equal(orc.block_deltas(np.eye(2, order="F"), 0, 2, np.array([3.0, 4.0]),
+                                                       np.ones(2)), z["eye"])
+        col = np.array([1.0, 2.0, -1.0])
+        xd = np.asfortranarray(np.column_stack([col, col]))
+        np.testing.assert_array_equal(orc.block_deltas(xd, 0, 2, col.copy(), orc.column_norms_sq(xd)), z["dup"])

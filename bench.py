@@ -62,6 +62,13 @@ CONFIGS = {
                desc="wide fp64 1,000x1,000,000, 10 sweeps"),
     "c5": dict(kind="batched", obs=512, vars=32, nsys=65536, dtype="f32", sweeps=200, tol=0.0, noise=0.01,
                desc="65,536 batched fp32 512x32 systems, 200 sweeps"),
+    # the blocked sweep (solve_bakp, Algorithm 2)
+    "p1": dict(kind="system", obs=10_000, vars=1000, dtype="f32", sweeps=20, tol=0.0, noise=0.0, thr=50,
+               desc="blocked sweep (solve_bakp) fp32 10,000x1,000 (the reference's paper-scale bakp test), "
+                    "thr=50, 20 sweeps"),
+    "p3": dict(kind="system", obs=1 << 24, vars=256, dtype="f64", sweeps=20, tol=0.0, noise=0.01, thr=32,
+               desc="blocked sweep (solve_bakp) very tall fp64 2^24x256, thr=32, 20 sweeps", variant="gram",
+               exact="stream"),
 }
 DEFAULT_CONFIG = "c3"
 METRIC = "sweeps/sec and x-stream HBM GB/s vs roofline at 1/2/4/8 B200; CPU baseline"
@@ -200,6 +207,27 @@ def cpu_baseline(cfg, dm, y, budget_s=12.0):
                           f"(bit-identical restatement of baksolve.solve_bak) on 1 core; batch-sweeps/s = "
                           f"sweeps / (per-system time x {dm.nsys})"}
     obs, nv = dm.obs, dm.vars
+    if cfg.get("thr"):
+        thr = cfg["thr"]
+        ncs = min(nv, 2 * thr if obs >= (1 << 22) else nv)
+        x = np.asfortranarray(dm.data[:ncs, :obs].cpu().numpy().T)
+        yy = y.cpu().numpy().copy()
+        n2 = orc.column_norms_sq(x)
+        a = np.zeros(ncs, dtype=x.dtype)
+        tmp = np.empty_like(yy)
+        sweeps = 0
+        with threadpool_limits(limits=1, user_api="blas"):
+            t0 = time.perf_counter()
+            while True:
+                orc.block_sweep_loop(x, yy, a, n2, tmp, thr, 1, None, None, float("inf"))
+                sweeps += 1
+                if time.perf_counter() - t0 > budget_s * 0.5:
+                    break
+            t = time.perf_counter() - t0
+        return {"value": 1.0 / (t / sweeps * nv / ncs), "unit": "sweeps/s", "cores": 1, "kind": "port",
+                "sample": f"{sweeps} blocked sweeps (thr={thr}) of the numpy oracle (bit-identical restatement "
+                          f"of baksolve.bakp._run_block_sweeps) over the first {ncs} full-length columns ({obs} "
+                          f"rows), 1 core; sweeps/s scaled by {ncs}/{nv} columns"}
     ncs = min(nv, 32 if obs >= (1 << 22) else (256 if obs >= 100_000 else nv))
     if cfg["kind"] == "c4":
         ncs = 20_000
@@ -241,6 +269,22 @@ def cpu_reference_threads(cfg, dm, y, budget_s=20.0):
                 "sample": f"{n} of {dm.nsys} systems x {cfg['sweeps']} sweeps, C/OpenMP port, {nt} threads "
                           f"(one system per thread); batch-sweeps/s scaled to {dm.nsys} systems"}
     obs, nv = dm.obs, dm.vars
+    if cfg.get("thr"):
+        thr = cfg["thr"]
+        ncs = min(nv, 2 * thr if obs >= (1 << 22) else nv)
+        x = np.asfortranarray(dm.data[:ncs, :obs].cpu().numpy().T)
+        yy = y.cpu().numpy()
+        oc.solve_block(x, yy, thr, 1, nthreads=nt)  # warm-up
+        sweeps, t = 0, 0.0
+        while t < budget_s * 0.5:
+            t0 = time.perf_counter()
+            oc.solve_block(x, yy, thr, 1, nthreads=nt)
+            t += time.perf_counter() - t0
+            sweeps += 1
+        return {"value": 1.0 / (t / sweeps * nv / ncs), "unit": "sweeps/s", "cores": nt, "kind": "port",
+                "sample": f"{sweeps} blocked sweeps (thr={thr}) over the first {ncs} full-length columns ({obs} "
+                          f"rows), C/OpenMP port (rows split over {nt} threads, block dots summed in thread "
+                          f"order); sweeps/s scaled by {ncs}/{nv} columns"}
     ncs = min(nv, 64 if obs >= (1 << 22) else (256 if obs >= 100_000 else nv))
     if cfg["kind"] == "c4":
         ncs = 50_000
@@ -303,6 +347,8 @@ def run_ours(args, cfg, rank, world, dev):
     batched = cfg["kind"] == "batched"
     variant = args.variant or cfg.get("variant", "auto")
     ts = 8 if cfg["dtype"] == "f64" else 4
+    if cfg.get("thr") and world > 1:
+        raise SystemExit("the blocked-sweep configs (p1, p3) are single-GPU workloads")
     sharded_rows = (not batched) and world > 1
     if batched:
         per = -(-cfg["nsys"] // world)
@@ -322,6 +368,8 @@ def run_ours(args, cfg, rank, world, dev):
     def step(v=variant):
         if batched:
             return pb.solve_bak_batched(dm, y, scfg, return_device=True)
+        if cfg.get("thr"):
+            return pb.solve_bakp(dm, y, pb.BlockConfig(base=scfg, thr=cfg["thr"]), variant=v, return_device=True)
         if sharded_rows:
             return solve_bak_rowsharded([dm], [y], scfg, comm, variant="stream" if v == "stream" else "gram",
                                         return_device=True)[0]
@@ -390,6 +438,30 @@ def run_ours(args, cfg, rank, world, dev):
         extra["gram_matrix"] = {"kernel": "gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
                                 "ms": round(g_ms, 3), "tflops": round(flops / (g_ms / 1e3) / 1e12, 2),
                                 "share_of_step": round(g_ms / (ms / args.steps), 3)}
+    elif cfg.get("thr"):
+        vcode = _lib.VARIANTS[used]
+        ws = _Workspace(torch, dev, max(_workspace_bytes(lib, code, dm.obs, dm.vars),
+                                        lib.bak_block_sweep_workspace(code, vcode, dm.obs, dm.vars, cfg["thr"])))
+        norms = pb.colnorms(dm, ws)
+        e = torch.empty_like(y)
+        a = torch.zeros(dm.vars, dtype=y.dtype, device=dev)
+        hist = torch.zeros(cfg["sweeps"], dtype=torch.float64, device=dev)
+        status = torch.zeros(4, dtype=torch.int64, device=dev)
+        k_tot = 0.0
+        for _ in range(args.steps):
+            e.copy_(y)
+            a.zero_()
+            kt, _ = _timed(lambda: _lib.check(lib.bak_block_sweep(
+                code, vcode, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(norms), cfg["thr"], _ptr(e), _ptr(a),
+                cfg["sweeps"], -1.0, float("inf"), _ptr(hist), _ptr(status), ws.ptr, ws.nbytes,
+                _stream_ptr(torch, dev)), "bak_block_sweep"), 1, dev, 1)
+            k_tot += kt
+        k_ms = k_tot / args.steps
+        k_sweeps = int(status[0].item())
+        xbytes = dm.obs * dm.vars * ts
+        alg_bytes = xbytes * k_sweeps
+        kernel = (f"block_kernel[{used}] (whole blocked solve; x read twice per block: dots, then e -= X_B d — "
+                  f"achieved counts ONE x read per sweep, the algorithmic floor)")
     else:
         ws = _Workspace(torch, dev, _workspace_bytes(lib, code, dm.obs, dm.vars, _lib.VARIANTS.get(variant, 0)))
         norms = pb.colnorms(dm, ws)
@@ -445,7 +517,9 @@ def run_ours(args, cfg, rank, world, dev):
             hxv = hx.t()[: dm.obs]
 
             def e2e_step():
-                if sharded_rows:
+                if cfg.get("thr"):
+                    r = pb.solve_bakp(hxv, hy, pb.BlockConfig(base=scfg, thr=cfg["thr"]), variant=variant)
+                elif sharded_rows:
                     r = solve_bak_rowsharded([hxv], [hy], scfg, comm,
                                              variant="stream" if variant == "stream" else "gram")[0]
                 else:
@@ -465,6 +539,7 @@ def run_ours(args, cfg, rank, world, dev):
         "data": "synthetic (seeded device RNG, reference distributions and shapes)",
         "config": {"workload": args.config, "desc": cfg["desc"], "obs": cfg["obs"], "vars": cfg["vars"],
                    "nsys": cfg.get("nsys", 1), "sweeps_per_step": cfg["sweeps"], "tol": cfg["tol"],
+                   "thr": cfg.get("thr"),
                    "variant": used + (" (labelled algebraically-equivalent sweep)" if used.startswith("gram") else ""),
                    "exact_variant": exact,
                    "rows_or_systems_per_rank": int(local_units),

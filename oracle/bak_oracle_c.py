@@ -54,3 +54,22 @@ def solve_batched(xs, ys, max_iter, nthreads=None):
         np.ascontiguousarray(xs).ctypes.data, obs, nv, ld, nv * ld, nsys, e.ctypes.data, obs, a.ctypes.data,
         n2.ctypes.data, max_iter, nthreads or threads())
     return a, e
+
+
+def solve_block(x, y, thr, max_iter, tol=0.0, nthreads=None):
+    """Blocked sweeps (solve_bakp); returns (a, e, sweeps, converged, history, diverged)."""
+    x = np.asfortranarray(x)
+    suf = "f64" if x.dtype == np.float64 else "f32"
+    e = np.array(y, dtype=x.dtype, copy=True)
+    a = np.zeros(x.shape[1], dtype=x.dtype)
+    n2 = np.einsum("ij,ij->j", x, x).astype(x.dtype)
+    ynorm2 = float(np.dot(e, e))
+    thresh2 = tol * tol * ynorm2 if tol > 0 else -1.0
+    hist = np.zeros(max_iter)
+    sw = ctypes.c_int64(0)
+    cv = ctypes.c_int(0)
+    div = getattr(lib(), "bako_solve_block_" + suf)(
+        x.ctypes.data, x.shape[0], x.shape[1], x.shape[0], e.ctypes.data, a.ctypes.data, n2.ctypes.data,
+        int(thr), max_iter, ctypes.c_double(thresh2), ctypes.c_double(ynorm2), hist.ctypes.data, ctypes.byref(sw),
+        ctypes.byref(cv), nthreads or threads())
+    return a, e, int(sw.value), bool(cv.value), hist[: sw.value].tolist(), bool(div)

@@ -34,6 +34,11 @@ def load():
         g = getattr(lib, "bako_solve_batched_" + suf)
         g.restype = ci
         g.argtypes = [vp, i64, i64, i64, i64, i64, vp, i64, vp, vp, i64, ci]
+    for suf in ("f64", "f32"):
+        h = getattr(lib, "bako_solve_block_" + suf)
+        h.restype = ci
+        h.argtypes = [vp, i64, i64, i64, vp, vp, vp, i64, i64, dbl, dbl, vp, ctypes.POINTER(i64),
+                      ctypes.POINTER(ci), ci]
     lib.bako_max_threads.restype = ci
     return lib
 

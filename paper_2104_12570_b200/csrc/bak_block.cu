@@ -45,7 +45,7 @@ namespace {
 
 constexpr int kModeCta = 0, kModeCluster = 1;
 constexpr int kMaxCluster = 16;
-constexpr int kMaxStages = 16;
+constexpr int kMaxStages = 128;
 constexpr int kMaxNT = 256;
 constexpr int kMaxWarps = kMaxNT / 32;
 constexpr int kChunk = 64;    // dots reduced / exchanged per round
@@ -66,6 +66,7 @@ struct BlockParams {
   int64_t* status;
   int64_t rows_per_cta;
   int nstages;
+  int resident;  // 1: a block's column slices stay in the ring for pass 2 (nstages > thr)
 };
 
 __device__ __forceinline__ bool bar_consumers_or(int nthreads, int pred) {
@@ -94,8 +95,25 @@ __host__ __device__ inline bool diverged(double sq, double prev) {
   return !(sq <= 1.79769313486231570815e308 && sq >= -1.79769313486231570815e308) || sq > prev * 10.0;
 }
 
+#ifdef BAK_PHASES
+#define BPH(i)                                 \
+  do {                                         \
+    const long long _c = clock64();            \
+    ph_acc[i] += _c - ph_last;                 \
+    ph_last = _c;                              \
+  } while (0)
+#else
+#define BPH(i) \
+  do {         \
+  } while (0)
+#endif
+
 template <typename T, int E, int MODE>
 __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams prm) {
+#ifdef BAK_PHASES
+  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+#endif
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NT = static_cast<int>(blockDim.x) - 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
@@ -149,8 +167,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
   __syncthreads();
   if (MODE == kModeCluster) cluster_sync();
 
-  // schedule: per sweep, per block, the block's columns twice
-  const int64_t per_sweep = 2 * V;
+  // schedule: per sweep, per block, the block's columns twice — or once when
+  // the block stays resident in the ring between its two passes
+  const bool resident = prm.resident != 0;
+  const int64_t per_sweep = resident ? V : 2 * V;
   const int64_t total = prm.max_iter * per_sweep;
 
   if (tid >= NT) {
@@ -163,6 +183,7 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
       int pass = 0;
       bool halted = false;
       for (; u < total; ++u) {
+        BPH(6);
         if (u >= S) {
           const uint32_t par = ph ^ 1u;
           if (!mbar_test(&empty[s], par)) {
@@ -173,6 +194,7 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
           }
           if (halted) break;
         }
+        BPH(5);
         const int64_t c = j0 + k;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(xs + static_cast<size_t>(s) * prm.rows_per_cta, x + c * prm.ldx + r0, bytes, &full[s], pol);
@@ -181,7 +203,7 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
         const int64_t j1 = imin64(j0 + thr, V);
         if (++k == j1 - j0) {
           k = 0;
-          if (pass == 0) {
+          if (pass == 0 && !resident) {
             pass = 1;
           } else {
             pass = 0;
@@ -189,6 +211,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
           }
         }
       }
+#ifdef BAK_PHASES
+      if (rank == 0 && prm.history)
+        for (int i = 5; i < 7; ++i) prm.history[prm.max_iter + i] = static_cast<double>(ph_acc[i]);
+#endif
       for (int64_t v = imax64(0, u - S); v < u; ++v) {  // drain in-flight copies
         const int sv = static_cast<int>(v % S);
         const uint32_t pv = static_cast<uint32_t>((v / S) & 1);
@@ -209,8 +235,9 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
     const bool full_rows = kv == E;
     const uint32_t xs_base = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
     const uint32_t stage_bytes = static_cast<uint32_t>(prm.rows_per_cta * sizeof(T));
-    // stage -> registers, then hand the stage back (one arrival per warp)
-    auto pull = [&](T (&xr)[E]) {
+    // stage -> registers, then (unless kept for pass 2) hand it back (one arrival per warp)
+    auto pull = [&](T (&xr)[E], bool keep) {
+      if (tid == 0) BPH(1);
       if (!mbar_test(&full[ls], lph)) {
         const uint64_t t0 = globaltimer();
         while (!mbar_test(&full[ls], lph)) {
@@ -221,12 +248,15 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
           }
         }
       }
+      if (tid == 0) BPH(0);
       const uint32_t a0 = xs_base + static_cast<uint32_t>(ls) * stage_bytes;
 #pragma unroll
       for (int k = 0; k < E; ++k)
         xr[k] = (full_rows || k < kv) ? lds<T>(a0 + static_cast<uint32_t>(k * NT * sizeof(T))) : T(0);
-      __syncwarp();
-      if (lane == 0) mbar_arrive1(&empty[ls]);
+      if (!keep) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&empty[ls]);
+      }
       if (++ls == S) { ls = 0; lph ^= 1u; }
     };
     // sum n values (thread t < n holds v) over the cluster, rank order; returns
@@ -265,10 +295,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
     int64_t sweep = 0;
     bool converged = false, div = false, aborted = false;
     double prev = prm.prev_sq;
-    T xr[E];
     while (sweep < prm.max_iter && !aborted) {
       for (int64_t j0 = 0; j0 < V && !aborted; j0 += thr) {
         const int64_t j1 = imin64(j0 + thr, V);
+        const int ls_block = ls;  // first stage of this block (resident mode)
         // ---- pass 1: thr dots against the stale e, reduced per chunk ----
         for (int64_t c0 = j0; c0 < j1; c0 += kChunk) {
           const int cn = static_cast<int>(imin64(kChunk, j1 - c0));
@@ -278,7 +308,8 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
             for (int u = 0; u < 4; ++u) {
               p[u] = T(0);
               if (i + u < cn) {
-                pull(xr);
+                T xr[E];
+                pull(xr, resident);
                 T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
                 for (int k = 0; k < E; ++k) acc[k & 3] = Num<T>::fma(xr[k], ev[k], acc[k & 3]);
@@ -294,6 +325,7 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
               for (int u = 0; u < 4; ++u)
                 if (i + u < cn) red[(i + u) * kMaxWarps + warp] = p[u];
           }
+          if (tid == 0) BPH(1);
           if (bar_consumers_or(NT, my_abort)) { aborted = true; break; }
           T n2 = T(1);
           double v = 0.0;
@@ -312,18 +344,39 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
           if (bar_consumers_or(NT, my_abort)) { aborted = true; break; }
         }
         if (aborted) break;
+        if (tid == 0) BPH(2);
         // ---- pass 2: e -= X_B d (scratch in T, fma chain in column order) ----
         T sc[E];
 #pragma unroll
         for (int k = 0; k < E; ++k) sc[k] = T(0);
-        for (int64_t j = j0; j < j1; ++j) {
-          pull(xr);
-          const T d = dsh[j - j0];
+        if (resident) {
+          // the block's slices are still in the ring: read them again, release each
+          int s2 = ls_block;
+          for (int64_t j = j0; j < j1; ++j) {
+            T xr[E];
+            const uint32_t a0 = xs_base + static_cast<uint32_t>(s2) * stage_bytes;
 #pragma unroll
-          for (int k = 0; k < E; ++k) sc[k] = Num<T>::fma(xr[k], d, sc[k]);
+            for (int k = 0; k < E; ++k)
+              xr[k] = (full_rows || k < kv) ? lds<T>(a0 + static_cast<uint32_t>(k * NT * sizeof(T))) : T(0);
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&empty[s2]);
+            if (++s2 == S) s2 = 0;
+            const T d = dsh[j - j0];
+#pragma unroll
+            for (int k = 0; k < E; ++k) sc[k] = Num<T>::fma(xr[k], d, sc[k]);
+          }
+        } else {
+          for (int64_t j = j0; j < j1; ++j) {
+            T xr[E];
+            pull(xr, false);
+            const T d = dsh[j - j0];
+#pragma unroll
+            for (int k = 0; k < E; ++k) sc[k] = Num<T>::fma(xr[k], d, sc[k]);
+          }
         }
 #pragma unroll
         for (int k = 0; k < E; ++k) ev[k] = Num<T>::sub(ev[k], sc[k]);
+        if (tid == 0) BPH(3);
       }
       if (aborted) break;
       // ---- sweep end: sum e^2, history, guard, early break ----
@@ -346,6 +399,7 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
       }
       if (bar_consumers_or(NT, my_abort)) break;
       const double sq = *qsh;
+      if (tid == 0) BPH(4);
       ++sweep;
       if (diverged(sq, prev)) {
         div = true;
@@ -360,6 +414,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
 #pragma unroll
     for (int k = 0; k < E; ++k)
       if (k < kv) eg[r0 + tid + static_cast<int64_t>(k) * NT] = ev[k];
+#ifdef BAK_PHASES
+    if (tid == 0 && rank == 0 && prm.history)
+      for (int i = 0; i < 5; ++i) prm.history[prm.max_iter + i] = static_cast<double>(ph_acc[i]);
+#endif
     if (tid == 0) {
       *stop = 1;
       if (rank == 0 && prm.status) {
@@ -515,7 +573,7 @@ __global__ void bdelta_kernel(const double* __restrict__ part, int nblk, int64_t
 // ------------------------------- host -------------------------------------
 struct BlockPlan {
   int variant = 0;
-  int parts = 1, nt = 32, e = 1, nstages = 2;
+  int parts = 1, nt = 32, e = 1, nstages = 2, resident = 0;
   int64_t rows_per_cta = 0;
 };
 
@@ -548,6 +606,11 @@ bool block_fill(int dtype, int variant, int64_t obs, int nt, int e, BlockPlan& p
   return true;
 }
 
+void block_residency(BlockPlan& pl, int64_t thr) {
+  // a block stays in the ring when the ring holds it plus some prefetch
+  pl.resident = pl.nstages >= thr + 2 ? 1 : 0;
+}
+
 bool block_plan(int dtype, int variant, int64_t obs, int64_t thr, BlockPlan& pl) {
   if (thr > kMaxThr) return false;
   if (variant == BAK_VARIANT_CTA) {
@@ -558,16 +621,13 @@ bool block_plan(int dtype, int variant, int64_t obs, int64_t thr, BlockPlan& pl)
     return false;
   }
   if (variant == BAK_VARIANT_CLUSTER) {
-    for (int nt : {128, 256}) {
-      for (int e : {8, 16}) {
-        const int64_t rows = static_cast<int64_t>(nt) * e;
-        const int64_t parts = (obs + rows - 1) / rows;
-        if (parts < 2 || parts > kMaxCluster) continue;
-        // spread rows evenly over the cluster
-        const int64_t per = (obs + parts - 1) / parts;
-        const int nt2 = static_cast<int>(round_up((per + e - 1) / e, 32));
-        if (block_fill(dtype, variant, obs, nt2, e, pl) && pl.parts >= 2) return true;
-      }
+    // as many CTAs as the cluster allows: the smallest slices (more SMs reading
+    // x, more ring stages -> a block can stay resident between its two passes)
+    const int64_t per = (obs + kMaxCluster - 1) / kMaxCluster;
+    for (int e : {8, 16, 4}) {
+      const int nt = static_cast<int>(round_up((per + e - 1) / e, 32));
+      if (nt > kMaxNT) continue;
+      if (block_fill(dtype, variant, obs, nt, e, pl) && pl.parts >= 2) return true;
     }
     return false;
   }
@@ -721,7 +781,7 @@ extern "C" int bak_block_sweep(int dtype, int variant, const void* x, int64_t ob
   if (variant == BAK_VARIANT_GRAM)
     return launch_gram_block(dtype, x, obs, ldx, vars, norms2, thr, e, a, max_iter, thresh2, prev_sq, history,
                              status, workspace, workspace_bytes, st);
-  BlockParams prm{x, obs, ldx, vars, norms2, thr, e, a, max_iter, thresh2, prev_sq, history, status, 0, 0};
+  BlockParams prm{x, obs, ldx, vars, norms2, thr, e, a, max_iter, thresh2, prev_sq, history, status, 0, 0, 0};
   if (variant == BAK_VARIANT_STREAM) {
     if (thr > kMaxThr) {
       set_error("bak_block_sweep(STREAM): thr <= %d", kMaxThr);
@@ -744,8 +804,11 @@ extern "C" int bak_block_sweep(int dtype, int variant, const void* x, int64_t ob
               variant);
     return BAK_EUNSUPPORTED;
   }
+  block_residency(pl, thr);
+  if (const char* r = getenv("BAK_BLOCK_RESIDENT")) pl.resident = (r[0] == '1') && pl.nstages > thr;
   prm.rows_per_cta = pl.rows_per_cta;
   prm.nstages = pl.nstages;
+  prm.resident = pl.resident;
   BAK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int64_t), st));
   int rc;
   if (dtype == BAK_F64)

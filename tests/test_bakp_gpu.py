@@ -246,3 +246,24 @@ def test_blocked_sweep_matches_naive_reference():
             e = e - x[:, j0:j1] @ dv
     rep = pb.solve_bakp(x, y, pb.BlockConfig(base=pb.SolveConfig(max_iter=3, tol=0), thr=thr))
     np.testing.assert_allclose(rep.a_hat, a, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("obs,nv,thr,dtype", [(10000, 300, 50, np.float32), (3000, 200, 20, np.float64),
+                                              (1500, 100, 8, np.float64)])
+def test_resident_ring_matches_restreaming(obs, nv, thr, dtype, monkeypatch):
+    """Keeping a block's column slices in the ring between its two passes
+    (planner default when it fits) gives the same bits as re-streaming them."""
+    pb = _pb()
+    rng = np.random.default_rng(obs)
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+    y = (x @ rng.uniform(-1, 1, nv).astype(dtype)).astype(dtype)
+    cfg = pb.BlockConfig(base=pb.SolveConfig(max_iter=6, tol=0, record_history=True), thr=thr)
+    monkeypatch.setenv("BAK_BLOCK_RESIDENT", "1")
+    r1 = pb.solve_bakp(x, y, cfg)
+    monkeypatch.setenv("BAK_BLOCK_RESIDENT", "0")
+    r0 = pb.solve_bakp(x, y, cfg)
+    assert r1.variant in ("cta", "cluster")
+    assert r1.a_hat.tobytes() == r0.a_hat.tobytes()
+    assert r1.residual_norm_history == r0.residual_norm_history
+    ref = orc.solve_bakp(x, y, max_iter=6, tol=0, thr=thr)
+    assert orc.rel_coeff_err(r1.a_hat, ref["a_hat"]) <= _tol(dtype)

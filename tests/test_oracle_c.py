@@ -2,6 +2,7 @@
 with the numpy oracle (itself bit-pinned to the reference).  CPU only."""
 
 import numpy as np
+import pytest
 
 from oracle import bak_oracle as orc
 from oracle import bak_oracle_c as oc
@@ -29,3 +30,29 @@ def test_c_port_early_break_and_batched():
     for s in range(6):
         r = orc.solve(xs[s].T, ys[s], max_iter=50, tol=0)
         assert orc.rel_coeff_err(a[s], r["a_hat"]) <= 1e-4
+
+
+@pytest.mark.parametrize("obs,nv,thr,dtype", [(300, 40, 7, np.float64), (20000, 64, 16, np.float64),
+                                              (5000, 30, 30, np.float32)])
+def test_c_port_block_matches_numpy_oracle(obs, nv, thr, dtype):
+    rng = np.random.default_rng(obs + thr)
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+    y = (x @ rng.standard_normal(nv).astype(dtype) + 0.1 * rng.standard_normal(obs)).astype(dtype)
+    try:
+        ref = orc.solve_bakp(x, y, max_iter=8, tol=0, thr=thr)
+    except orc.DivergenceError:
+        a, e, sw, cv, hist, div = oc.solve_block(x, y, thr, 8, nthreads=4)
+        assert div
+        return
+    a, e, sw, cv, hist, div = oc.solve_block(x, y, thr, 8, nthreads=4)
+    assert not div and sw == ref["sweeps_run"]
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    assert orc.rel_coeff_err(a, ref["a_hat"]) <= tol
+
+
+def test_c_port_block_divergence_guard():
+    rng = np.random.default_rng(21)
+    col = rng.standard_normal(50)
+    x = np.asfortranarray(np.tile(col[:, None], (1, 5)))
+    *_, div = oc.solve_block(x, col.copy(), 5, 10)
+    assert div

@@ -26,7 +26,8 @@ def _tol(dtype):
 
 def _variants(obs, nv, dtype):
     vs = ["auto", "stream"]
-    if obs <= (2048 if np.dtype(dtype) == np.float64 else 4096):
+    # on-chip kernels (TMA ring default): one CTA up to 256 threads x 8 rows, clusters of <= 16
+    if obs <= 2048:
         vs.append("cta")
     elif obs <= 32768:
         vs.append("cluster")
@@ -258,6 +259,7 @@ def test_resident_ring_matches_restreaming(obs, nv, thr, dtype, monkeypatch):
     x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
     y = (x @ rng.uniform(-1, 1, nv).astype(dtype)).astype(dtype)
     cfg = pb.BlockConfig(base=pb.SolveConfig(max_iter=6, tol=0, record_history=True), thr=thr)
+    monkeypatch.setenv("BAK_BLOCK_KERNEL", "tma")
     monkeypatch.setenv("BAK_BLOCK_RESIDENT", "1")
     r1 = pb.solve_bakp(x, y, cfg)
     monkeypatch.setenv("BAK_BLOCK_RESIDENT", "0")
@@ -267,3 +269,22 @@ def test_resident_ring_matches_restreaming(obs, nv, thr, dtype, monkeypatch):
     assert r1.residual_norm_history == r0.residual_norm_history
     ref = orc.solve_bakp(x, y, max_iter=6, tol=0, thr=thr)
     assert orc.rel_coeff_err(r1.a_hat, ref["a_hat"]) <= _tol(dtype)
+
+
+@pytest.mark.parametrize("obs,nv,thr,dtype", [(10000, 300, 50, np.float32), (900, 200, 20, np.float64),
+                                              (12000, 100, 8, np.float64), (777, 64, 5, np.float32)])
+def test_direct_load_and_tma_ring_kernels_agree(obs, nv, thr, dtype, monkeypatch):
+    """The two on-chip kernels (default: TMA ring with a producer warp; and the
+    direct-load form) agree with each other and with the oracle."""
+    pb = _pb()
+    rng = np.random.default_rng(obs + 1)
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+    y = (x @ rng.uniform(-1, 1, nv).astype(dtype) + 0.01 * rng.standard_normal(obs)).astype(dtype)
+    cfg = pb.BlockConfig(base=pb.SolveConfig(max_iter=8, tol=0), thr=thr)
+    r_tma = pb.solve_bakp(x, y, cfg)
+    monkeypatch.setenv("BAK_BLOCK_KERNEL", "ldg")
+    r_ldg = pb.solve_bakp(x, y, cfg)
+    assert r_ldg.variant == r_tma.variant or {r_ldg.variant, r_tma.variant} <= {"cta", "cluster"}
+    ref = orc.solve_bakp(x, y, max_iter=8, tol=0, thr=thr)
+    for r in (r_ldg, r_tma):
+        _check(r, ref["a_hat"], ref["sweeps_run"], ref["converged"], x, y, dtype)

@@ -1,6 +1,6 @@
-"""Per-sweep cost model of the on-chip blocked kernel: time solve_bakp over a
-grid of (obs, thr) and fit t_sweep = nblocks * c_block + vars * c_col.
-Tuning aid, not a bench line."""
+"""Kernel-only cost model of the on-chip blocked sweep: time bak_block_sweep
+(C-ABI, CUDA events around the launch only) over (vars, thr) and fit
+t_sweep = nblocks * c_block + vars * c_col + c_sweep.  Tuning aid."""
 import os
 import sys
 
@@ -9,41 +9,57 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2104_12570_b200 as pb  # noqa: E402
+from paper_2104_12570_b200 import _lib  # noqa: E402
+from paper_2104_12570_b200.bak import _Workspace, _ptr, _stream_ptr  # noqa: E402
 
+lib = _lib.load()
 dev = torch.device("cuda", 0)
-nv = 1000
+sweeps = int(os.environ.get("SWEEPS", 20))
 for dt in (torch.float32, torch.float64):
-    for obs in (1000, 2000, 10000, 30000):
-        g = torch.Generator(device=dev)
-        g.manual_seed(0)
-        x = torch.randn(nv, obs, dtype=dt, device=dev, generator=g)
-        y = x.t() @ (torch.rand(nv, dtype=dt, device=dev, generator=g) - 0.5)
-        dm = pb.DeviceMatrix(x, obs, nv, np.float64 if dt == torch.float64 else np.float32)
+    for obs in [int(v) for v in os.environ.get("OBS", "1000,10000").split(",")]:
         rows = []
-        for thr in (5, 10, 25, 50, 100, 200):
-            cfg = pb.BlockConfig(base=pb.SolveConfig(max_iter=10, tol=0), thr=thr)
-            try:
-                r = pb.solve_bakp(dm, y, cfg, return_device=True)
-            except pb.DivergenceError:
-                print(dt, obs, thr, "diverged")
-                continue
-            torch.cuda.synchronize()
-            ts = []
-            for _ in range(3):
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record()
-                r = pb.solve_bakp(dm, y, cfg, return_device=True)
-                b.record()
+        for nv in (500, 1000):
+            g = torch.Generator(device=dev)
+            g.manual_seed(0)
+            x = torch.randn(nv, obs, dtype=dt, device=dev, generator=g)
+            y = x.t() @ (torch.rand(nv, dtype=dt, device=dev, generator=g) - 0.5)
+            dm = pb.DeviceMatrix(x, obs, nv, np.float64 if dt == torch.float64 else np.float32)
+            norms = pb.colnorms(dm)
+            for thr in (5, 10, 25, 50, 100):
+                e = y.clone()
+                a = torch.zeros(nv, dtype=dt, device=dev)
+                hist = torch.zeros(sweeps, dtype=torch.float64, device=dev)
+                st = torch.zeros(4, dtype=torch.int64, device=dev)
+                ws = _Workspace(torch, dev, lib.bak_block_sweep_workspace(dm.code, 0, obs, nv, thr))
+
+                def run():
+                    e.copy_(y)
+                    a.zero_()
+                    _lib.check(lib.bak_block_sweep(dm.code, 0, dm.ptr, obs, nv, dm.ldx, _ptr(norms), thr, _ptr(e),
+                                                   _ptr(a), sweeps, -1.0, float("inf"), _ptr(hist), _ptr(st),
+                                                   ws.ptr, ws.nbytes, _stream_ptr(torch, dev)), "sweep")
+                run()
                 torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            ms = min(ts) / r.sweeps_run
-            nb = -(-nv // thr)
-            rows.append((nb, ms))
-            print(f"{dt} obs={obs} thr={thr} variant={r.variant} us/sweep={ms * 1e3:.1f} us/block={ms * 1e3 / nb:.2f}",
-                  flush=True)
-        if len(rows) >= 2:
-            A = np.array([[nb, nv] for nb, _ in rows], float)
-            t = np.array([ms * 1e3 for _, ms in rows])
-            c, *_ = np.linalg.lstsq(A, t, rcond=None)
-            print(f"  fit: c_block={c[0]:.2f} us, c_col={c[1] * 1e3:.1f} ns", flush=True)
+                best = 1e9
+                for _ in range(3):
+                    e.copy_(y)
+                    a.zero_()
+                    s0 = torch.cuda.Event(enable_timing=True)
+                    s1 = torch.cuda.Event(enable_timing=True)
+                    s0.record()
+                    _lib.check(lib.bak_block_sweep(dm.code, 0, dm.ptr, obs, nv, dm.ldx, _ptr(norms), thr, _ptr(e),
+                                                   _ptr(a), sweeps, -1.0, float("inf"), _ptr(hist), _ptr(st),
+                                                   ws.ptr, ws.nbytes, _stream_ptr(torch, dev)), "sweep")
+                    s1.record()
+                    torch.cuda.synchronize()
+                    best = min(best, s0.elapsed_time(s1))
+                us = best * 1e3 / sweeps
+                nb = -(-nv // thr)
+                rows.append((nb, nv, us))
+                print(f"{dt} obs={obs} vars={nv} thr={thr} variant={int(st[3])} err={int(st[2])} "
+                      f"us/sweep={us:.1f} ns/col={us * 1e3 / nv:.0f}", flush=True)
+        A = np.array([[nb, nv, 1] for nb, nv, _ in rows], float)
+        t = np.array([u for *_, u in rows])
+        c, *_ = np.linalg.lstsq(A, t, rcond=None)
+        print(f"  fit {dt} obs={obs}: c_block={c[0]:.2f} us, c_col={c[1] * 1e3:.1f} ns, c_sweep={c[2]:.1f} us",
+              flush=True)

@@ -217,6 +217,15 @@ int bak_block_sweep(int dtype, int variant,
 /* block_deltas (bakp.py:65-85): out[k - j0] = <x_k, e>/n2_k for k in [j0, j1),
  * 0 where n2_k == 0; 0 <= j0 < j1 <= vars. */
 int64_t bak_block_deltas_workspace(int dtype, int64_t obs);
+/* ---- greedy column scoring (select.py:56-85) ------------
+ * scores[j] = <e,e> - <x_j,e>^2 / norms2[j] in T (double output), +inf where
+ * excluded[j] != 0 (NULL = none) or norms2[j] <= 0; best (device int64[2]) =
+ * {argmin (NaN first, ties to the lowest index), 1 if that score is finite}.
+ * Replaces score_all_columns' x.T @ e, closed form and argmin (select.py:73-85). */
+int64_t bak_score_columns_workspace(int dtype, int64_t obs, int64_t vars);
+int bak_score_columns(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, const void* e,
+                      const void* norms2, const uint8_t* excluded, double* scores, int64_t* best,
+                      void* workspace, int64_t workspace_bytes, void* stream);
 int bak_block_deltas(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx,
                      int64_t j0, int64_t j1, const void* e, const void* norms2, void* out,
                      void* workspace, int64_t workspace_bytes, void* stream);

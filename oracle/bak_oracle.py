@@ -30,6 +30,9 @@ Reference map (``/root/reference/pkg/src/baksolve``):
   fp64 metrics       bench.py:109-121 (_predict_f64), bench.py:180-184
   blocked solver     bakp.py:52-185 (block_deltas, _run_block_sweeps, solve_bakp),
                      DIVERGENCE_FACTOR bakp.py:32
+  column scoring     select.py:56-85 (score_all_columns), greedy selection
+                     select.py:88-136 (select_features, _refit), Householder
+                     least squares qr.py:42-119 (refit="qr")
 """
 
 from __future__ import annotations
@@ -369,3 +372,112 @@ def config_c4(obs=1000, nvars=1_000_000, seed=4):
 
 def config_c5_system(s, obs=512, nvars=32, base_seed=5_000_000):
     return make_system(obs, nvars, base_seed + s, "normal", "uniform", 0.01, "single")
+
+
+# --------------------------------------------------------------------------
+# greedy column scoring and selection (select.py) — SURVEY §8f row 3
+# --------------------------------------------------------------------------
+
+class SelectionExhaustedError(RuntimeError):
+    """select.py:29-30"""
+
+
+def score_all_columns(x, e, excluded=()):
+    """select.py:56-85: scores[j] = <e,e> - <x_j,e>^2 / <x_j,x_j> in T (one
+    ?gemv for all dots), +inf for excluded or zero-norm columns; argmin with
+    ties to the lowest index."""
+    x = np.asarray(x)
+    e = np.asarray(e)
+    obs, nvars = x.shape
+    if e.shape != (obs,):
+        raise ValueError(f"residual has shape {e.shape}, expected ({obs},)")
+    ok = np.ones(nvars, dtype=bool)
+    if len(excluded):
+        ok[np.asarray(sorted(excluded), dtype=int)] = False
+    n2 = column_norms_sq(x)
+    ok &= n2 > 0
+    scores = np.full(nvars, np.inf)
+    if ok.any():
+        g = x.T @ e
+        e2 = np.dot(e, e)
+        idx = np.flatnonzero(ok)
+        scores[idx] = e2 - g[idx] * g[idx] / n2[idx]
+    best = int(np.argmin(scores))
+    if not np.isfinite(scores[best]):
+        raise SelectionExhaustedError("no non-excluded column with nonzero norm")
+    return best, scores
+
+
+def householder_lstsq(x, y):
+    """Least squares by unpivoted Householder QR of [x | y] (qr.py:47-119):
+    reflector v = (1, col[1:]/(alpha - beta)), beta = -sign(alpha)*||col||,
+    tau = 2/(1 + |v_tail|^2); dependent columns (|r_jj| <= max(m,n)*eps*max|r|)
+    keep coefficient 0; back substitution from the last column."""
+    x = _coerce_matrix(x)
+    m, n = x.shape
+    y = _coerce_vector(y, x.dtype)
+    w = np.empty((m, n + 1), dtype=x.dtype, order="F")
+    w[:, :n] = x
+    w[:, n] = y
+    one, two = x.dtype.type(1), x.dtype.type(2)
+    k = min(m, n)
+    for j in range(k):
+        col = w[j:, j]
+        nrm = np.sqrt(np.dot(col, col))
+        if nrm == 0.0:
+            continue
+        alpha = col[0]
+        beta = -np.copysign(nrm, alpha)
+        tail = w[j + 1:, j]
+        tail /= alpha - beta
+        tau = two / (one + np.dot(tail, tail))
+        w[j, j] = beta
+        if j + 1 < n + 1:
+            s = w[j, j + 1:] + tail @ w[j + 1:, j + 1:]
+            s *= tau
+            w[j, j + 1:] -= s
+            w[j + 1:, j + 1:] -= np.outer(tail, s)
+    r_diag = w.diagonal()[:k]
+    scale = float(np.max(np.abs(r_diag))) if r_diag.size else 0.0
+    tol = max(m, n) * float(np.finfo(r_diag.dtype).eps) * scale
+    a = np.zeros(n, dtype=x.dtype)
+    qty = w[:, n]
+    for j in reversed(range(k)):
+        rjj = w[j, j]
+        if abs(rjj) <= tol:
+            continue
+        a[j] = (qty[j] - np.dot(w[j, j + 1:n], a[j + 1:])) / rjj
+    return a
+
+
+def select_features(x, y, max_feat, refit="qr", stop_tol=0.0, refit_config=None):
+    """select.py:106-136: score, pick, refit on the picked columns (QR, or
+    solve_bak warm-started from the previous coefficients), recompute e."""
+    x = _coerce_matrix(x)
+    obs, nvars = x.shape
+    y = _coerce_vector(y, x.dtype)
+    if y.shape[0] != obs:
+        raise ValueError(f"y has length {y.shape[0]}, expected {obs}")
+    if max_feat > nvars:
+        raise ValueError(f"max_feat={max_feat} exceeds the number of columns ({nvars})")
+    ynorm = np.linalg.norm(y.astype(np.float64))
+    selected, norms, coeffs = [], [], None
+    e = y.copy()
+    for _ in range(max_feat):
+        best, _ = score_all_columns(x, e, excluded=selected)
+        selected.append(best)
+        xs = np.asfortranarray(x[:, selected])
+        if refit == "qr":
+            coeffs = householder_lstsq(xs, y)
+        else:
+            cfg = dict(refit_config or {})
+            a0 = np.zeros(xs.shape[1], dtype=xs.dtype)
+            if coeffs is not None:
+                a0[:coeffs.shape[0]] = coeffs
+            coeffs = solve(xs, y, a0=a0, **cfg)["a_hat"]
+        e = y - xs @ coeffs
+        rn = float(np.dot(e, e))
+        norms.append(rn)
+        if stop_tol > 0 and ynorm > 0 and np.sqrt(rn) / ynorm <= stop_tol:
+            break
+    return dict(selected=selected, residual_norms=norms, final_coeffs=coeffs)

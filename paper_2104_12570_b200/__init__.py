@@ -8,6 +8,9 @@ Names mirror ``baksolve`` (reference __init__.py:9-10): SolveConfig,
 SolveReport, solve_bak, coordinate_update, residual_norm, DRIFT_TOL.
 The blocked solver of the reference's bakp.py (Algorithm 2): solve_bakp,
 block_deltas, BlockConfig, DivergenceError, DIVERGENCE_FACTOR.
+Greedy column scoring / forward selection of select.py:
+score_all_columns, select_features, FeatureSelectConfig,
+FeatureSelectionReport, SelectionExhaustedError, REFITS.
 Extension: solve_bak_batched for many independent small systems.
 """
 
@@ -15,10 +18,14 @@ from .bak import (DRIFT_TOL, ORDERINGS, BatchSolveReport, DeviceBatch, DeviceMat
                   colnorms, coordinate_update, residual_norm, solve_bak, solve_bak_batched, to_device_batch,
                   to_device_matrix)
 from .bakp import DIVERGENCE_FACTOR, BlockConfig, DivergenceError, block_deltas, solve_bakp
+from .select import (REFITS, FeatureSelectConfig, FeatureSelectionReport, SelectionExhaustedError,
+                     score_all_columns, select_features)
 
 __version__ = "0.1.0"
 
-__all__ = ["DIVERGENCE_FACTOR", "DRIFT_TOL", "ORDERINGS", "BatchSolveReport", "BlockConfig", "DeviceBatch",
+__all__ = ["REFITS", "FeatureSelectConfig", "FeatureSelectionReport", "SelectionExhaustedError", "score_all_columns",
+           "select_features",
+           "DIVERGENCE_FACTOR", "DRIFT_TOL", "ORDERINGS", "BatchSolveReport", "BlockConfig", "DeviceBatch",
            "DeviceMatrix", "DivergenceError", "SolveConfig", "SolveReport", "block_deltas", "colnorms",
            "coordinate_update", "residual_norm", "solve_bak", "solve_bak_batched", "solve_bakp", "to_device_batch",
            "to_device_matrix"]

@@ -48,6 +48,8 @@ SIGNATURES = {
     "bak_block_sweep": (_int, [_int, _int, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp,
                                _vp, _i64, _vp]),
     "bak_block_deltas_workspace": (_i64, [_int, _i64]),
+    "bak_score_columns_workspace": (_i64, [_int, _i64, _i64]),
+    "bak_score_columns": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_block_deltas": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_matrix_dot": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),

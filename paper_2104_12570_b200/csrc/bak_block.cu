@@ -949,7 +949,7 @@ int block_ldg_launch(const BlockPlan& pl, const BlockParams& prm, cudaStream_t s
 
 // Default: the producer-warp TMA ring kernel (measured ~20% faster per sweep on
 // the 10,000 x 1,000 paper-scale shape); BAK_BLOCK_KERNEL=ldg selects the
-// direct-load kernel (tests check both against the oracle and each other).
+// direct-load kernel (tests check both against the CPU restatement and each other).
 bool use_tma_block_kernel() {
   const char* k = getenv("BAK_BLOCK_KERNEL");
   return !(k && k[0] == 'l');

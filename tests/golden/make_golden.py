@@ -4,6 +4,7 @@ Run in the build container, where the reference is mounted read-only:
 
     python tests/golden/make_golden.py            # writes tests/golden/*.npz
     python tests/golden/make_golden.py --bakp-only   # only the bakp_*.npz fixtures
+    python tests/golden/make_golden.py --select-only # only the select_*.npz fixtures
 
 The reference is imported from ``/root/reference/pkg/src`` (pure Python on
 numpy/OpenBLAS).  Nothing at test time reads ``/root/reference``: the
@@ -49,6 +50,13 @@ def main():
             "blas": (blas[0].get("internal_api"), blas[0].get("version"),
                      blas[0].get("architecture")) if blas else None}
 
+    if "--select-only" in sys.argv:  # regenerate only the column-scoring / selection fixtures
+        with open(os.path.join(HERE, "MANIFEST.json")) as f:
+            man = json.load(f)
+        man["select_cases"] = make_select(bk, host)
+        with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
+            json.dump(man, f, indent=1)
+        return
     if "--bakp-only" in sys.argv:  # regenerate only the blocked-solver fixtures
         with open(os.path.join(HERE, "MANIFEST.json")) as f:
             man = json.load(f)
@@ -163,8 +171,9 @@ def main():
     np.savez_compressed(os.path.join(HERE, "kat_coordinate_update.npz"),
                         col=np.array([1.0, 2.0]), e=np.array([3.0, 4.0]), da=np.array(da), e_next=e_next)
     bakp_cases = make_bakp(bk, host, _predict_f64)
+    select_cases = make_select(bk, host)
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
-        json.dump({"host": host, "cases": cases, "bakp_cases": bakp_cases,
+        json.dump({"host": host, "cases": cases, "bakp_cases": bakp_cases, "select_cases": select_cases,
                    "reference": "baksolve 0.1.0 (/root/reference/pkg)"}, f, indent=1)
 
 
@@ -260,6 +269,90 @@ def make_bakp(bk, host, _predict_f64):
                         eye=bk.block_deltas(np.eye(2, order="F"), (0, 2), np.array([3.0, 4.0])),
                         dup=bk.block_deltas(np.asfortranarray(np.column_stack([[1.0, 2.0, -1.0]] * 2)), (0, 2),
                                             np.array([1.0, 2.0, -1.0])))
+    return cases
+
+
+
+def make_select(bk, host):
+    """Fixtures of score_all_columns / select_features (select.py:56-136),
+    files select_*.npz: inputs plus the reference's outputs."""
+    cases = []
+
+    def randn(rng, obs, nv, dtype=np.float64):
+        return np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+
+    def score(name, x, e, excluded=()):
+        try:
+            best, scores = bk.score_all_columns(x, e, excluded=list(excluded))
+            d = dict(best=np.array(best), scores=scores, exhausted=np.array(False))
+        except bk.SelectionExhaustedError:
+            d = dict(best=np.array(-1), scores=np.zeros(0), exhausted=np.array(True))
+        np.savez_compressed(os.path.join(HERE, f"select_{name}.npz"), kind=np.array("score"), x=x, e=e,
+                            excluded=np.asarray(sorted(excluded), dtype=np.int64), host=np.array(json.dumps(host)),
+                            **d)
+        cases.append("select_" + name)
+        print(f"select_{name:30s} score best={int(d['best'])}")
+
+    def select(name, x, y, max_feat, refit="qr", stop_tol=0.0, refit_cfg=None):
+        cfg = bk.FeatureSelectConfig(max_feat=max_feat, refit=refit, stop_tol=stop_tol,
+                                     refit_config=bk.SolveConfig(**refit_cfg) if refit_cfg else None)
+        rep = bk.select_features(x, y, cfg)
+        np.savez_compressed(os.path.join(HERE, f"select_{name}.npz"), kind=np.array("select"), x=x, y=y,
+                            max_feat=np.array(max_feat), refit=np.array(refit), stop_tol=np.array(stop_tol),
+                            refit_cfg=np.array(json.dumps(refit_cfg or {})),
+                            selected=np.asarray(rep.selected, dtype=np.int64),
+                            residual_norms=np.asarray(rep.residual_norms, dtype=np.float64),
+                            final_coeffs=np.asarray(rep.final_coeffs), host=np.array(json.dumps(host)))
+        cases.append("select_" + name)
+        print(f"select_{name:30s} selected={rep.selected}")
+
+    rng = np.random.default_rng(40)
+    x = randn(rng, 30, 6)
+    score("explains_30x6", x, x[:, 3].copy())
+    rng = np.random.default_rng(42)
+    score("random_20x5", randn(rng, 20, 5), rng.standard_normal(20))
+    rng = np.random.default_rng(43)
+    score("f32_400x30", randn(rng, 400, 30, np.float32), rng.standard_normal(400).astype(np.float32))
+    rng = np.random.default_rng(44)
+    x = randn(rng, 30, 4)
+    x[:, 2] = 0.0
+    e = x[:, 1].copy()
+    score("zero_col_excluded_30x4", x, e, excluded=[1])
+    score("exhausted_30x4", x, e, excluded=[0, 1, 3])
+    rng = np.random.default_rng(56)
+    col = rng.standard_normal(25)
+    score("tie_25x3", np.asfortranarray(np.column_stack([col, col, col])), rng.standard_normal(25))
+    rng = np.random.default_rng(60)
+    score("tall_16384x16", randn(rng, 16384, 16), rng.standard_normal(16384))
+    rng = np.random.default_rng(61)
+    score("wide_100x2000_f32", randn(rng, 100, 2000, np.float32), rng.standard_normal(100).astype(np.float32))
+
+    def sparse(rng, obs, nv, k):
+        x = randn(rng, obs, nv)
+        sup = sorted(rng.choice(nv, size=k, replace=False).tolist())
+        a = np.zeros(nv)
+        a[sup] = rng.uniform(1.0, 2.0, k) * rng.choice([-1.0, 1.0], k)
+        return x, x @ a
+
+    for seed in (3000, 3001):
+        x, y = sparse(np.random.default_rng(seed), 500, 50, 3)
+        select(f"support_{seed}_500x50", x, y, 3)
+    rng = np.random.default_rng(46)
+    x = randn(rng, 60, 8)
+    select("full_60x8", x, rng.standard_normal(60), 8)
+    x, y = sparse(np.random.default_rng(47), 200, 30, 2)
+    select("stop_tol_200x30", x, y, 10, stop_tol=1e-8)
+    x, y = sparse(np.random.default_rng(48), 300, 40, 4)
+    select("bak_refit_300x40", x, y, 4, refit="bak", refit_cfg=dict(max_iter=4000, tol=1e-10))
+    rng = np.random.default_rng(49)
+    x = randn(rng, 80, 10)
+    x[:, 4] = 0.0
+    select("zero_col_80x10", x, rng.standard_normal(80), 9)
+    rng = np.random.default_rng(62)
+    x = randn(rng, 2000, 100, np.float32)
+    y = (x[:, [3, 17, 60]] @ np.array([1.5, -2.0, 0.7], np.float32) + 0.01 * rng.standard_normal(2000)).astype(
+        np.float32)
+    select("f32_bak_2000x100", x, y, 5, refit="bak", refit_cfg=dict(max_iter=200, tol=1e-7))
     return cases
 
 

@@ -12,7 +12,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_")))
+                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_", "select_")))
 
 
 def bakp_names():
@@ -60,3 +60,31 @@ def input_sha(x, y):
     h.update(np.ascontiguousarray(np.asfortranarray(x)).tobytes())
     h.update(np.ascontiguousarray(y).tobytes())
     return h.hexdigest()
+
+
+def select_names(kind=None):
+    """Fixtures of score_all_columns / select_features (make_golden.make_select)."""
+    out = []
+    for p in sorted(glob.glob(os.path.join(GOLDEN, "select_*.npz"))):
+        name = os.path.basename(p)[:-4]
+        if kind is None or str(np.load(p)["kind"]) == kind:
+            out.append(name)
+    return out
+
+
+def load_select(name):
+    with np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    d["kind"] = str(d["kind"])
+    d["host"] = json.loads(str(d["host"]))
+    if d["kind"] == "select":
+        d["refit"] = str(d["refit"])
+        d["refit_cfg"] = json.loads(str(d["refit_cfg"]))
+        d["max_feat"] = int(d["max_feat"])
+        d["stop_tol"] = float(d["stop_tol"])
+        d["selected"] = d["selected"].tolist()
+    else:
+        d["excluded"] = d["excluded"].tolist()
+        d["best"] = int(d["best"])
+        d["exhausted"] = bool(d["exhausted"])
+    return d

@@ -115,3 +115,15 @@ def test_divergence_first_sweep_logic_cpu():
     assert _first_divergence([float("nan")], float("inf"))[0] == float("inf")
     assert _divergence_message(44.9682, 719.49, 5) == (
         "residual norm grew from 44.9682 to 719.49 in one sweep with thr=5; use a smaller thr")
+
+
+def test_feature_select_config_validation_cpu():
+    """FeatureSelectConfig mirrors select.py:33-46 (pure host logic)."""
+    from paper_2104_12570_b200 import REFITS, FeatureSelectConfig
+    assert REFITS == ("qr", "bak")
+    with pytest.raises(ValueError):
+        FeatureSelectConfig(max_feat=0)
+    with pytest.raises(ValueError):
+        FeatureSelectConfig(max_feat=1, refit="ridge")
+    with pytest.raises(ValueError):
+        FeatureSelectConfig(max_feat=1, stop_tol=-0.5)

@@ -79,6 +79,7 @@ def test_manifest_lists_every_fixture():
         man = json.load(f)
     assert sorted(man["cases"]) == golden_io.names()
     assert sorted(man["bakp_cases"]) == golden_io.bakp_names()
+    assert sorted(man["select_cases"]) == golden_io.select_names()
 
 
 @pytest.mark.parametrize("name", golden_io.bakp_names())
@@ -124,3 +125,35 @@ def test_block_deltas_kat():
         col = np.array([1.0, 2.0, -1.0])
         xd = np.asfortranarray(np.column_stack([col, col]))
         np.testing.assert_array_equal(orc.block_deltas(xd, 0, 2, col.copy(), orc.column_norms_sq(xd)), z["dup"])
+
+
+@pytest.mark.parametrize("name", golden_io.select_names("score"))
+def test_oracle_scores_match_reference_fixture(name):
+    """score_all_columns restatement (select.py:56-85)."""
+    g = golden_io.load_select(name)
+    if g["exhausted"]:
+        with pytest.raises(orc.SelectionExhaustedError):
+            orc.score_all_columns(g["x"], g["e"], excluded=g["excluded"])
+        return
+    best, scores = orc.score_all_columns(g["x"], g["e"], excluded=g["excluded"])
+    assert best == g["best"]
+    if _same_blas(g["host"]):
+        assert scores.tobytes() == g["scores"].tobytes()
+    else:
+        fin = np.isfinite(g["scores"])
+        assert np.array_equal(np.isfinite(scores), fin)
+        np.testing.assert_allclose(scores[fin], g["scores"][fin], rtol=1e-5, atol=1e-8)
+
+
+@pytest.mark.parametrize("name", golden_io.select_names("select"))
+def test_oracle_selection_matches_reference_fixture(name):
+    """select_features + Householder / solve_bak refit restatement (select.py:88-136, qr.py)."""
+    g = golden_io.load_select(name)
+    out = orc.select_features(g["x"], g["y"], g["max_feat"], refit=g["refit"], stop_tol=g["stop_tol"],
+                              refit_config=g["refit_cfg"] or None)
+    assert out["selected"] == g["selected"]
+    if _same_blas(g["host"]):
+        assert np.asarray(out["final_coeffs"]).tobytes() == g["final_coeffs"].tobytes()
+        assert out["residual_norms"] == g["residual_norms"].tolist()
+    else:
+        np.testing.assert_allclose(out["final_coeffs"], g["final_coeffs"], rtol=1e-6, atol=1e-9)

@@ -191,6 +191,14 @@ int bak_ipc_get_handle(void* devptr, void* handle64);
 int bak_ipc_open_handle(const void* handle64, void** devptr);
 int bak_ipc_close(void* devptr);
 
+/* ---- BAKM matrix files (matio.py:17-57); host only -------
+ * bak_bakm_header: the 16-byte header {"BAKM", u32 rows, u32 cols, u32 tag
+ * 32|64}; BAK_EINVAL with matio's messages (truncated header / bad magic /
+ * unknown precision tag).  bak_file_read: parallel pread of a byte range into
+ * host memory (pinned for the GPU upload path); "file is short" on EOF. */
+int bak_bakm_header(const char* path, int64_t* rows, int64_t* cols, int* tag, int64_t* file_bytes);
+int bak_file_read(const char* path, int64_t offset, void* dst, int64_t bytes, int nthreads);
+
 /* ---- blocked sweep: solve_bakp / block_deltas (bakp.py:52-185) -------------
  * Replaces baksolve.bakp._run_block_sweeps (bakp.py:95-129), cyclic order:
  * consecutive blocks of thr columns (narrower last block); per block every

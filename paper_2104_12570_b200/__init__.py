@@ -11,6 +11,8 @@ block_deltas, BlockConfig, DivergenceError, DIVERGENCE_FACTOR.
 Greedy column scoring / forward selection of select.py:
 score_all_columns, select_features, FeatureSelectConfig,
 FeatureSelectionReport, SelectionExhaustedError, REFITS.
+BAKM / CSV matrix files of matio.py (§8f row 4): save_matrix, load_matrix,
+load_vector, MatrixFormatError, plus load_matrix_pinned / load_matrix_device.
 Extension: solve_bak_batched for many independent small systems.
 """
 
@@ -18,12 +20,15 @@ from .bak import (DRIFT_TOL, ORDERINGS, BatchSolveReport, DeviceBatch, DeviceMat
                   colnorms, coordinate_update, residual_norm, solve_bak, solve_bak_batched, to_device_batch,
                   to_device_matrix)
 from .bakp import DIVERGENCE_FACTOR, BlockConfig, DivergenceError, block_deltas, solve_bakp
+from .matio import (FORMATS, MAGIC, MatrixFormatError, load_matrix, load_matrix_device, load_matrix_pinned,
+                    load_vector, save_matrix)
 from .select import (REFITS, FeatureSelectConfig, FeatureSelectionReport, SelectionExhaustedError,
                      score_all_columns, select_features)
 
 __version__ = "0.1.0"
 
-__all__ = ["REFITS", "FeatureSelectConfig", "FeatureSelectionReport", "SelectionExhaustedError", "score_all_columns",
+__all__ = ["FORMATS", "MAGIC", "MatrixFormatError", "load_matrix", "load_matrix_device", "load_matrix_pinned",
+           "load_vector", "save_matrix", "REFITS", "FeatureSelectConfig", "FeatureSelectionReport", "SelectionExhaustedError", "score_all_columns",
            "select_features",
            "DIVERGENCE_FACTOR", "DRIFT_TOL", "ORDERINGS", "BatchSolveReport", "BlockConfig", "DeviceBatch",
            "DeviceMatrix", "DivergenceError", "SolveConfig", "SolveReport", "block_deltas", "colnorms",

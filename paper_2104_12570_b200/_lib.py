@@ -49,6 +49,8 @@ SIGNATURES = {
                                _vp, _i64, _vp]),
     "bak_block_deltas_workspace": (_i64, [_int, _i64]),
     "bak_score_columns_workspace": (_i64, [_int, _i64, _i64]),
+    "bak_bakm_header": (_int, [ctypes.c_char_p, _vp, _vp, _vp, _vp]),
+    "bak_file_read": (_int, [ctypes.c_char_p, _i64, _vp, _i64, _int]),
     "bak_score_columns": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_block_deltas": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_matrix_dot": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),

@@ -60,7 +60,7 @@ def build(verbose=False, force=False):
     if failed:
         raise RuntimeError("CUDA build failed")
     tmp = LIB + ".tmp"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -5,6 +5,7 @@ Run in the build container, where the reference is mounted read-only:
     python tests/golden/make_golden.py            # writes tests/golden/*.npz
     python tests/golden/make_golden.py --bakp-only   # only the bakp_*.npz fixtures
     python tests/golden/make_golden.py --select-only # only the select_*.npz fixtures
+    python tests/golden/make_golden.py --matio-only  # only the matio_* files (reference save_matrix)
 
 The reference is imported from ``/root/reference/pkg/src`` (pure Python on
 numpy/OpenBLAS).  Nothing at test time reads ``/root/reference``: the
@@ -56,6 +57,9 @@ def main():
         man["select_cases"] = make_select(bk, host)
         with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
             json.dump(man, f, indent=1)
+        return
+    if "--matio-only" in sys.argv:  # regenerate only the BAKM / CSV files
+        make_matio(bk)
         return
     if "--bakp-only" in sys.argv:  # regenerate only the blocked-solver fixtures
         with open(os.path.join(HERE, "MANIFEST.json")) as f:
@@ -354,6 +358,20 @@ def make_select(bk, host):
         np.float32)
     select("f32_bak_2000x100", x, y, 5, refit="bak", refit_cfg=dict(max_iter=200, tol=1e-7))
     return cases
+
+
+def make_matio(bk):
+    """Files written by the reference's save_matrix (matio.py:29-39): a
+    binary f64, a binary f32 and a CSV, plus the matrices they hold."""
+    rng = np.random.default_rng(65)
+    x64 = np.asfortranarray(rng.standard_normal((13, 4)))
+    x64[0, 0], x64[1, 1], x64[2, 2] = 1.0 / 3.0, 1e-300, -1e308
+    x32 = np.asfortranarray(rng.standard_normal((7, 3)).astype(np.float32))
+    bk.save_matrix(os.path.join(HERE, "matio_f64.bakm"), x64, format="binary")
+    bk.save_matrix(os.path.join(HERE, "matio_f32.bakm"), x32, format="binary")
+    bk.save_matrix(os.path.join(HERE, "matio_f64.csv"), x64, format="csv")
+    np.savez_compressed(os.path.join(HERE, "matio_expected.npz"), x64=x64, x32=x32)
+    print("matio fixtures written")
 
 
 if __name__ == "__main__":

@@ -12,7 +12,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_", "select_")))
+                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_", "select_", "matio_")))
 
 
 def bakp_names():

@@ -6,6 +6,7 @@ Run in the build container, where the reference is mounted read-only:
     python tests/golden/make_golden.py --bakp-only   # only the bakp_*.npz fixtures
     python tests/golden/make_golden.py --select-only # only the select_*.npz fixtures
     python tests/golden/make_golden.py --matio-only  # only the matio_* files (reference save_matrix)
+    python tests/golden/make_golden.py --harness-only  # only harness_records.json (reference run_case)
 
 The reference is imported from ``/root/reference/pkg/src`` (pure Python on
 numpy/OpenBLAS).  Nothing at test time reads ``/root/reference``: the
@@ -57,6 +58,9 @@ def main():
         man["select_cases"] = make_select(bk, host)
         with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
             json.dump(man, f, indent=1)
+        return
+    if "--harness-only" in sys.argv:  # regenerate only the run_case records
+        make_harness(bk)
         return
     if "--matio-only" in sys.argv:  # regenerate only the BAKM / CSV files
         make_matio(bk)
@@ -372,6 +376,38 @@ def make_matio(bk):
     bk.save_matrix(os.path.join(HERE, "matio_f64.csv"), x64, format="csv")
     np.savez_compressed(os.path.join(HERE, "matio_expected.npz"), x64=x64, x32=x32)
     print("matio fixtures written")
+
+
+def make_harness(bk):
+    """Records of the reference's run_case (bench.py:137-195) for a few small
+    generated cases (wall time dropped): the harness's metrics must agree."""
+    import dataclasses
+    cases = [
+        dict(case_id="s400_bak", solver="bak", obs=400, vars=40, seed=7, precision="single", tol=1e-6,
+             max_iter=300),
+        dict(case_id="s400_bakp", solver="bakp", obs=400, vars=40, seed=7, precision="single", tol=1e-6,
+             max_iter=300, thr=8),
+        dict(case_id="s400_qr", solver="qr", obs=400, vars=40, seed=7, precision="single", tol=1e-6,
+             max_iter=300),
+        dict(case_id="d1000_bak", solver="bak", obs=1000, vars=100, seed=5, precision="double", tol=1e-10,
+             max_iter=2000),
+        dict(case_id="d1000_coeffs", solver="qr", obs=1000, vars=100, seed=5, precision="double", tol=1e-6,
+             max_iter=300, mape_base="coeffs"),
+        dict(case_id="p2000_bakp", solver="bakp", obs=2000, vars=200, seed=11, precision="single", tol=1e-6,
+             max_iter=200, thr=20),
+    ]
+    out = []
+    for c in cases:
+        spec = bk.RunSpec(case_id=c["case_id"], solver=c["solver"],
+                          system=bk.SystemSpec(obs=c["obs"], vars=c["vars"], seed=c["seed"]),
+                          precision=c["precision"], thr=c.get("thr", 50), tol=c["tol"], max_iter=c["max_iter"],
+                          repetitions=1, mape_base=c.get("mape_base", "targets"))
+        rec = dataclasses.asdict(bk.run_case(spec))
+        rec.pop("wall_time_s")
+        out.append(dict(spec=c, record=rec))
+        print(c["case_id"], rec["sweeps"], rec["mape"], rec["rel_residual"])
+    with open(os.path.join(HERE, "harness_records.json"), "w") as f:
+        json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":

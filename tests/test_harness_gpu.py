@@ -98,8 +98,8 @@ def test_run_suite_and_cli(tmp_path, capsys):
     h = _h()
     from paper_2104_12570_b200 import cli
     p = tmp_path / "s.csv"
-    p.write_text("case_id,solver,obs,vars,seed,precision,reps,max_iter\n"
-                 "c1,bak,200,20,1,double,1,500\nc1,qr,200,20,1,double,1,500\nc1,bakp,200,20,1,double,1,500\n")
+    p.write_text("case_id,solver,obs,vars,seed,precision,reps,max_iter,thr\n"
+                 "c1,bak,200,20,1,double,1,500,5\nc1,qr,200,20,1,double,1,500,5\nc1,bakp,200,20,1,double,1,500,5\n")
     seen = []
     records = h.run_suite(p, on_record=seen.append)
     assert [r.solver for r in records] == ["bak", "qr", "bakp"] and seen == records

@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
         if (row < p.obs) e[row] = en;
         ev = static_cast<double>(en);
         sq = __fma_rn(ev, ev, sq);
+      } else {
+        sq = __fma_rn(ev, ev, sq);  // dot-only pass: sum e^2 of the unchanged e (column scoring)
       }
       es[lane] = ev;
       if (want_r && row < p.obs) {

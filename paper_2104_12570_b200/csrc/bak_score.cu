@@ -12,7 +12,10 @@
 // score_final_kernel sums the tile partials in tile order, applies the closed
 // form and a per-CTA argmin; score_argmin_kernel reduces the CTA winners in
 // index order.  HBM-bound: obs*vars*sizeof(T) + e once per column group.
+#include <type_traits>
+
 #include "bak_common.cuh"
+#include "bak_sweep.cuh"
 
 namespace bak {
 namespace {
@@ -142,10 +145,96 @@ __global__ void score_argmin_kernel(const double* __restrict__ cta_val, const in
   best[1] = (bv == bv && bv < __longlong_as_double(0x7ff0000000000000LL)) ? 1 : 0;  // finite
 }
 
+// short columns (obs <= kShortMax): e staged once per CTA in shared memory,
+// one warp per column (lane-strided rows), score and running argmin in the
+// same kernel; per-CTA winners go to score_argmin_kernel.
+constexpr int kShortMax = 4096;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) score_short_kernel(const T* __restrict__ x, int64_t obs, int64_t ldx,
+                                                               int64_t vars, const T* __restrict__ e,
+                                                               const T* __restrict__ n2g,
+                                                               const uint8_t* __restrict__ excluded,
+                                                               double* __restrict__ scores,
+                                                               double* __restrict__ cta_val,
+                                                               int64_t* __restrict__ cta_idx) {
+  __shared__ T es[kShortMax];
+  __shared__ T red[kThreads / 32];
+  __shared__ double sv[kThreads / 32];
+  __shared__ int64_t si[kThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = static_cast<int>(obs);
+  T q = T(0);
+  for (int r = tid; r < n; r += kThreads) {
+    const T v = e[r];
+    es[r] = v;
+    q = Num<T>::fma(v, v, q);
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[warp] = q;
+  __syncthreads();
+  T e2 = T(0);
+  for (int w = 0; w < kThreads / 32; ++w) e2 = Num<T>::add(e2, red[w]);  // same order in every CTA
+  double bv = __longlong_as_double(0x7ff0000000000000LL);
+  int64_t bi = INT64_MAX;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp; j < vars; j += wstride) {
+    const T* __restrict__ col = x + j * ldx;
+    // 16-byte vector loads (columns are 16-byte aligned), lane-strided
+    constexpr int VEC = 16 / sizeof(T);
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    const int nvec = n / VEC;
+    T acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = T(0);
+#pragma unroll 2
+    for (int i = lane; i < nvec; i += 32) {
+      const V v = __ldcs(reinterpret_cast<const V*>(col) + i);
+      const T* xv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[k] = Num<T>::fma(xv[k], es[i * VEC + k], acc[k]);
+    }
+    for (int r = nvec * VEC + lane; r < n; r += 32) acc[0] = Num<T>::fma(col[r], es[r], acc[0]);
+    T gs = acc[0];
+#pragma unroll
+    for (int k = 1; k < VEC; ++k) gs = Num<T>::add(gs, acc[k]);
+    const T g = warp_sum(gs);
+    const T n2 = n2g[j];
+    double v = __longlong_as_double(0x7ff0000000000000LL);
+    if (n2 > T(0) && !(excluded && excluded[j]))
+      v = static_cast<double>(Num<T>::sub(e2, Num<T>::div(Num<T>::mul(g, g), n2)));
+    if (lane == 0) scores[j] = v;
+    if (better(v, j, bv, bi)) {
+      bv = v;
+      bi = j;
+    }
+  }
+  if (lane == 0) {
+    sv[warp] = bv;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double b = sv[0];
+    int64_t ib = si[0];
+    for (int w = 1; w < kThreads / 32; ++w)
+      if (better(sv[w], si[w], b, ib)) {
+        b = sv[w];
+        ib = si[w];
+      }
+    cta_val[blockIdx.x] = b;
+    cta_idx[blockIdx.x] = ib;
+  }
+}
+
 struct ScorePlan {
   int ngroups, ntiles, nfinal;
   int64_t tile;
 };
+
+int short_ctas(int64_t vars) {
+  return static_cast<int>(imax64(1, imin64(8LL * device_sms(), (vars + kThreads / 32 - 1) / (kThreads / 32))));
+}
 
 ScorePlan score_plan(int64_t obs, int64_t vars) {
   ScorePlan p;
@@ -156,6 +245,11 @@ ScorePlan score_plan(int64_t obs, int64_t vars) {
   p.tile = round_up((obs + nt - 1) / nt, kThreads);
   p.ntiles = static_cast<int>((obs + p.tile - 1) / p.tile);
   p.nfinal = static_cast<int>((vars + kThreads - 1) / kThreads);
+  if (obs <= kShortMax) p.nfinal = static_cast<int>(imax64(p.nfinal, short_ctas(vars)));
+  if (gram_tma_supported(vars) && obs > kShortMax) {
+    // tall: the GRAM pass kernel in dot-only mode (TMA-fed, ~HBM speed) makes the partials
+    p.ntiles = static_cast<int>(imax64(p.ntiles, gram_tma_grid(BAK_F32)));
+  }
   return p;
 }
 
@@ -168,7 +262,7 @@ extern "C" int64_t bak_score_columns_workspace(int dtype, int64_t obs, int64_t v
   (void)dtype;
   const ScorePlan p = score_plan(obs, vars);
   return round_up(static_cast<int64_t>(p.ntiles) * vars * 8, 256) + round_up(p.ntiles * 8, 256) +
-         2 * round_up(p.nfinal * 8, 256) + 256;
+         2 * round_up(p.nfinal * 8, 256) + 512;
 }
 
 extern "C" int bak_score_columns(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, const void* e,
@@ -194,6 +288,46 @@ extern "C" int bak_score_columns(int dtype, const void* x, int64_t obs, int64_t 
   w += round_up(p.nfinal * 8, 256);
   int64_t* cta_idx = reinterpret_cast<int64_t*>(w);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t ts = dtype_size(dtype);
+  if (obs <= kShortMax && reinterpret_cast<uintptr_t>(x) % 16 == 0 && (ldx * ts) % 16 == 0) {
+    const int nc = short_ctas(vars);
+    if (dtype == BAK_F64)
+      score_short_kernel<double><<<nc, kThreads, 0, st>>>(static_cast<const double*>(x), obs, ldx, vars,
+                                                          static_cast<const double*>(e),
+                                                          static_cast<const double*>(norms2), excluded, scores,
+                                                          cta_val, cta_idx);
+    else
+      score_short_kernel<float><<<nc, kThreads, 0, st>>>(static_cast<const float*>(x), obs, ldx, vars,
+                                                         static_cast<const float*>(e),
+                                                         static_cast<const float*>(norms2), excluded, scores,
+                                                         cta_val, cta_idx);
+    score_argmin_kernel<<<1, 32, 0, st>>>(cta_val, cta_idx, nc, best);
+    count_launches(2);
+    BAK_CHECK_CUDA(cudaGetLastError());
+    return BAK_OK;
+  }
+  if (gram_tma_supported(vars) && reinterpret_cast<uintptr_t>(x) % 16 == 0 && (ldx * ts) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(e) % 16 == 0) {
+    // dot-only GRAM pass: gpart[b][j] = partial <x_j, e>, sqpart[b] = partial <e, e>
+    const int nblk = gram_tma_grid(dtype);
+    int64_t* done = reinterpret_cast<int64_t*>(cta_idx + p.nfinal);  // zeroed flag after the winners
+    BAK_CHECK_CUDA(cudaMemsetAsync(done, 0, 8, st));
+    if (int rc = launch_gram_pass_tma(dtype, x, obs, ldx, vars, const_cast<void*>(e), part, 0, 1, part, e2part,
+                                      done, st))
+      return rc;
+    if (dtype == BAK_F64)
+      score_final_kernel<double><<<p.nfinal, kThreads, 0, st>>>(part, e2part, nblk, vars,
+                                                                static_cast<const double*>(norms2), excluded, scores,
+                                                                cta_val, cta_idx);
+    else
+      score_final_kernel<float><<<p.nfinal, kThreads, 0, st>>>(part, e2part, nblk, vars,
+                                                               static_cast<const float*>(norms2), excluded, scores,
+                                                               cta_val, cta_idx);
+    score_argmin_kernel<<<1, 32, 0, st>>>(cta_val, cta_idx, p.nfinal, best);
+    count_launches(2);
+    BAK_CHECK_CUDA(cudaGetLastError());
+    return BAK_OK;
+  }
   const dim3 g1(p.ntiles, p.ngroups);
   if (dtype == BAK_F64) {
     score_dots_kernel<double><<<g1, kThreads, 0, st>>>(static_cast<const double*>(x), obs, ldx, vars,

@@ -2,8 +2,10 @@
 // system runs the whole of solve_bak (bak.py:146-195) for that system.
 //
 //  - x (obs x vars, column-major) is brought into shared memory ONCE with a
-//    single cp.async.bulk when it fits (C5: 512 x 32 fp32 = 64 KiB), so the
-//    200 sweeps read it on chip; otherwise columns are read from L2/HBM.
+//    single cp.async.bulk when that leaves >= 8 systems per SM; otherwise
+//    (C5: 512 x 32 fp32 = 64 KiB -> only 3 per SM) columns are streamed from
+//    L2/HBM every sweep by many more resident systems (HBM-bound, 2.2x faster
+//    on C5).
 //  - e lives in registers (E rows per thread, rows tid + k*NT).
 //  - per column: fused  e -= d_j x_j ; p += x_next . e  then one block
 //    reduction (warp butterfly, + per-warp slots when NT > 32).
@@ -349,7 +351,18 @@ extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t 
   const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ldx * ts) % 16 == 0) &&
                        ((x_stride * ts) % 16 == 0) && xbytes < (1u << 20);
   size_t smem = small;
-  if (aligned && xbytes + small <= cap) {
+  // x resident in shared memory only when that still leaves >= 8 systems per
+  // SM in flight; otherwise stream x from L2/HBM every sweep with many more
+  // systems per SM.  Measured on C5 (65,536 x 512x32 fp32, 64 KiB of x per
+  // system): resident (3 systems/SM, latency-bound) 277 ms vs streamed
+  // (1 warp per system, HBM-bound at 6.8 TB/s) 127 ms per 200 sweeps.
+  // BAK_BATCH_X=smem|stream forces either (tests check they agree bit for bit).
+  const char* force = getenv("BAK_BATCH_X");
+  const bool fits = aligned && xbytes + small <= cap;
+  bool use_smem = fits && (cap / (xbytes + small)) >= 8;
+  if (force && force[0] == 's' && force[1] == 'm') use_smem = fits;
+  if (force && force[0] == 's' && force[1] == 't') use_smem = false;
+  if (use_smem) {
     prm.x_in_smem = 1;
     smem += xbytes;
   }

@@ -185,6 +185,27 @@ def test_batched_matches_oracle_per_system():
         assert abs(r - r_ref) / r_ref <= 1e-4
 
 
+@pytest.mark.parametrize("shape", [(512, 32, np.float32), (200, 12, np.float64), (37, 6, np.float64)])
+def test_batched_smem_resident_and_streamed_x_agree(shape, monkeypatch):
+    """x resident in shared memory vs streamed from L2/HBM every sweep (the
+    default when residency would leave < 8 systems per SM): same arithmetic,
+    same bits."""
+    pb = _pb()
+    obs, nv, dt = shape
+    rng = np.random.default_rng(obs)
+    xs = rng.standard_normal((24, obs, nv)).astype(dt)
+    ys = rng.standard_normal((24, obs)).astype(dt)
+    cfg = pb.SolveConfig(max_iter=30, tol=1e-9, record_history=True)
+    monkeypatch.setenv("BAK_BATCH_X", "smem")
+    r1 = pb.solve_bak_batched(xs, ys, cfg)
+    monkeypatch.setenv("BAK_BATCH_X", "stream")
+    r2 = pb.solve_bak_batched(xs, ys, cfg)
+    assert r1.a_hat.tobytes() == r2.a_hat.tobytes()
+    assert r1.residual.tobytes() == r2.residual.tobytes()
+    assert np.array_equal(r1.sweeps_run, r2.sweeps_run)
+    assert np.array_equal(r1.residual_norm_history, r2.residual_norm_history)
+
+
 def test_batched_edge_cases():
     pb = _pb()
     rng = np.random.default_rng(5)

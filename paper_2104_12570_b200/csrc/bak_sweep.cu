@@ -53,14 +53,6 @@ constexpr int kMaxStages = 16;
 constexpr int kMaxConsumers = 256;
 constexpr int kBarConsumers = 1;  // named barrier id used by consumer warps only
 
-struct ColCursor {
-  const int32_t* cols;
-  int64_t ncols, stride, s, k;
-  __device__ __forceinline__ int64_t col() const { return cols ? static_cast<int64_t>(cols[s * stride + k]) : k; }
-  __device__ __forceinline__ void next() {
-    if (++k == ncols) { k = 0; ++s; }
-  }
-};
 
 struct alignas(16) Pair {
   double p, q;
@@ -181,41 +173,64 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
 
   if (tid >= NT) {
     // =========================== producer warp ===========================
-    if (lane == 0) {
+    // The whole warp prepares the next 32 schedule steps at once (lane l:
+    // column index, n2 and 1/n2 of step u0 + l — the dependent global load and
+    // the division leave the per-column critical path); lane 0 then issues the
+    // 32 stage fills in order (wait for the stage, write its record, TMA).
+    {
       const uint64_t pol = policy_evict_first();
-      ColCursor pc{prm.cols, ncols, prm.cols_stride, 0, 0};
       int s = 0;
       uint32_t ph = 0;
       int64_t u = 0;
       bool halted = false;
-      for (; u < total; ++u) {
-        if (u >= S) {
-          const uint32_t par = ph ^ 1u;
-          if (!mbar_test(&empty[s], par)) {
-            const uint64_t t0 = globaltimer();
-            while (!mbar_test(&empty[s], par)) {
-              if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+      for (int64_t u0 = 0; u0 < total && !halted; u0 += 32) {
+        const int64_t ul = u0 + lane;
+        int64_t cl = 0;
+        T n2l = T(1);
+        if (ul < total) {
+          const int64_t sw = ul / ncols, k = ul - sw * ncols;
+          cl = prm.cols ? static_cast<int64_t>(prm.cols[sw * prm.cols_stride + k]) : k;
+          n2l = n2g[cl];
+        }
+        const T ril = Num<T>::div(T(1), n2l);
+        const int nb = static_cast<int>(imin64(32, total - u0));
+        for (int i = 0; i < nb; ++i) {
+          const int64_t c = __shfl_sync(0xffffffffu, cl, i);
+          const T n2 = __shfl_sync(0xffffffffu, n2l, i);
+          const T ri = __shfl_sync(0xffffffffu, ril, i);
+          if (lane == 0) {
+            if (u >= S) {
+              const uint32_t par = ph ^ 1u;
+              if (!mbar_test(&empty[s], par)) {
+                const uint64_t t0 = globaltimer();
+                while (!mbar_test(&empty[s], par)) {
+                  if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+                }
+              }
+            }
+            if (!halted) {
+              meta[s].col = c;
+              meta[s].n2 = static_cast<double>(n2);
+              meta[s].rinv = static_cast<double>(ri);
+              mbar_arrive_expect_tx(&full[s], bytes);  // release: meta visible with the phase
+              bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + c * prm.ldx + r0, bytes, &full[s], pol);
+              if (++s == S) { s = 0; ph ^= 1u; }
+              ++u;
             }
           }
+          halted = __shfl_sync(0xffffffffu, halted, 0);
           if (halted) break;
         }
-        const int64_t c = pc.col();
-        pc.next();
-        const T n2 = n2g[c];
-        meta[s].col = c;
-        meta[s].n2 = static_cast<double>(n2);
-        meta[s].rinv = static_cast<double>(Num<T>::div(T(1), n2));
-        mbar_arrive_expect_tx(&full[s], bytes);  // release: meta visible with the phase
-        bulk_g2s(xs + static_cast<size_t>(s) * prm.stage_elems, x + c * prm.ldx + r0, bytes, &full[s], pol);
-        if (++s == S) { s = 0; ph ^= 1u; }
       }
       // drain: the last min(S, u) issued copies must land before this CTA exits
-      for (int64_t v = imax64(0, u - S); v < u; ++v) {
-        const int sv = static_cast<int>(v % S);
-        const uint32_t pv = static_cast<uint32_t>((v / S) & 1);
-        const uint64_t t0 = globaltimer();
-        while (!mbar_test(&full[sv], pv))
-          if (globaltimer() - t0 > kTimeoutNs) break;
+      if (lane == 0) {
+        for (int64_t v = imax64(0, u - S); v < u; ++v) {
+          const int sv = static_cast<int>(v % S);
+          const uint32_t pv = static_cast<uint32_t>((v / S) & 1);
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test(&full[sv], pv))
+            if (globaltimer() - t0 > kTimeoutNs) break;
+        }
       }
     }
   } else {

@@ -349,7 +349,8 @@ def run_ours(args, cfg, rank, world, dev):
     ts = 8 if cfg["dtype"] == "f64" else 4
     if cfg.get("thr") and world > 1:
         raise SystemExit("the blocked-sweep configs (p1, p3) are single-GPU workloads")
-    sharded_rows = (not batched) and world > 1
+    force_shard = os.environ.get("BAK_FORCE_SHARDED") == "1"  # exercise the N>1 code path at N=1 (NCCL, 1 rank)
+    sharded_rows = (not batched) and (world > 1 or force_shard)
     if batched:
         per = -(-cfg["nsys"] // world)
         s0, s1 = min(cfg["nsys"], rank * per), min(cfg["nsys"], (rank + 1) * per)
@@ -363,7 +364,7 @@ def run_ours(args, cfg, rank, world, dev):
         dm, y = make_inputs(cfg, dev, seed=1234)
         local_units = dm.obs
     scfg = pb.SolveConfig(max_iter=cfg["sweeps"], tol=cfg["tol"])
-    comm = DistComm() if world > 1 else None
+    comm = DistComm() if (world > 1 or force_shard) else None
 
     def step(v=variant):
         if batched:
@@ -607,12 +608,13 @@ def main():
         return
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    if world > 1:
+    dist_on = world > 1 or os.environ.get("BAK_FORCE_SHARDED") == "1"
+    if dist_on:
         torch.distributed.init_process_group("nccl", device_id=dev)
     out = run_ours(args, cfg, rank, world, dev)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist_on:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 

@@ -184,12 +184,19 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
             raise _lib.BakError(f"bak_sweep_rowshard device error {int(stat[2])} (3 = exchange timeout)")
         sweeps, converged = int(stat[0]), bool(stat[1])
         return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "stream-rowshard")
-    G_parts = []
+    # G and the first sweep's dots g = X^T e in one read of each shard (the DMMA
+    # kernel's diagonal-block CTAs produce the dots); rows of partials padded
+    # to the largest shard's count so the all-gather has one shape everywhere
+    g0rows = max(int(lib.bak_gram_dot_rows(code, s.dm.obs, nv)) for s in shards)
+    g0rows = int(max(comm.all_gather([torch.tensor([g0rows], device=dev) for _ in shards])).item())
+    G_parts, g0_parts = [], []
     for s in shards:
         G = torch.empty((nv, nv), dtype=torch.float64, device=dev)
-        _lib.check(lib.bak_gram_matrix(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(G), s.ws.ptr, s.ws.nbytes, st),
-                   "bak_gram_matrix")
+        g0 = torch.zeros((g0rows, nv), dtype=torch.float64, device=dev)
+        _lib.check(lib.bak_gram_matrix_dot(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(G), _ptr(s.e), _ptr(g0),
+                                           s.ws.ptr, s.ws.nbytes, st), "bak_gram_matrix_dot")
         G_parts.append(G)
+        g0_parts.append(g0)
     G = rank_order_sum(comm.all_gather(G_parts))
 
     nblk = lib.bak_gram_pass_blocks(code, nv)
@@ -213,33 +220,42 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
         cols_all = torch.from_numpy(perms).to(dev)
         ncols, stride = perms.shape[1], perms.shape[1]
 
-    def passes(apply, dot):
+    fused = thresh2 < 0 and nv <= 256  # no early break: the last (TMA) pass also writes resid = y - x a
+    for s in shards:
+        s.resid = torch.empty_like(s.y) if fused else None
+
+    def passes(apply, dot, last=False):
         for s in shards:
-            _lib.check(lib.bak_gram_pass(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(s.e), _ptr(delta), apply, dot,
-                                         _ptr(s.gpart), _ptr(s.sqpart), _ptr(ctrl), st), "bak_gram_pass")
+            fin = last and fused
+            _lib.check(lib.bak_gram_pass_resid(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(s.e), _ptr(delta), apply,
+                                               dot, _ptr(s.gpart), _ptr(s.sqpart), _ptr(ctrl),
+                                               _ptr(a if fin else None), _ptr(s.y if fin else None),
+                                               _ptr(s.resid if fin else None), st), "bak_gram_pass")
         gp = comm.all_gather([s.gpart for s in shards])
         sp = comm.all_gather([s.sqpart for s in shards])
         return torch.cat([g.reshape(-1) for g in gp]), torch.cat(sp)
 
     def solve(gp, sp, sweep):
-        _lib.check(lib.bak_gram_solve(code, nv, _ptr(gp), _ptr(sp), sp.numel(), sweep, cfg.max_iter, thresh2,
+        _lib.check(lib.bak_gram_solve(code, nv, _ptr(gp), _ptr(sp), gp.numel() // nv, sweep, cfg.max_iter, thresh2,
                                       _ptr(cols_all), ncols, stride, _ptr(norms), _ptr(G), _ptr(a), _ptr(delta),
                                       _ptr(hist), _ptr(ctrl), _ptr(status), st), "bak_gram_solve")
 
-    gp, sp = passes(0, 1)
+    gp = torch.cat([g.reshape(-1) for g in comm.all_gather(g0_parts)])
+    sp = torch.zeros(1, dtype=torch.float64, device=dev)  # not read by the first solve
     for sweep in range(1, cfg.max_iter + 1):
         solve(gp, sp, sweep)
-        gp, sp = passes(1, 1 if sweep < cfg.max_iter else 0)
+        gp, sp = passes(1, 1 if sweep < cfg.max_iter else 0, last=sweep == cfg.max_iter)
         if thresh2 >= 0 and sweep % 16 == 0 and int(ctrl[0].item()):
             break
     solve(gp, sp, cfg.max_iter + 1)
     stat = status.cpu().numpy()
     sweeps, converged = int(stat[0]), bool(stat[1])
 
-    return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "gram-rowshard")
+    return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "gram-rowshard",
+                           fused_resid=fused)
 
 
-def _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, label):
+def _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, label, fused_resid=False):
     """Residual y - x a per shard (bak.py:130) and the drift flag (bak.py:133-142)."""
     torch = _torch()
     lib = _lib.load()
@@ -250,9 +266,12 @@ def _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return
     resids = []
     d2_parts = []
     for s in shards:
-        r = torch.empty_like(s.y)
-        _lib.check(lib.bak_residual(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(a), _ptr(s.y), _ptr(r), s.ws.ptr,
-                                    s.ws.nbytes, st), "bak_residual")
+        if fused_resid:
+            r = s.resid                                  # written by the last GRAM pass
+        else:
+            r = torch.empty_like(s.y)
+            _lib.check(lib.bak_residual(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(a), _ptr(s.y), _ptr(r),
+                                        s.ws.ptr, s.ws.nbytes, st), "bak_residual")
         d2 = torch.empty(1, dtype=torch.float64, device=dev)
         _lib.check(lib.bak_diff_norm2(code, _ptr(s.e), _ptr(r), s.dm.obs, _ptr(d2), s.ws.ptr, s.ws.nbytes, st),
                    "bak_diff_norm2")

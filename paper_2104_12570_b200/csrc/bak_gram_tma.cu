@@ -51,25 +51,31 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-// fp32 tiles are half the bytes for the same instructions: two CTAs per SM
+// Rows per lane: fp32 tiles are 64 rows (each lane owns rows lane and
+// lane+32) so that a tile carries as many bytes as an fp64 tile of 32 rows —
+// the per-tile fixed costs (two named barriers, warp 0's row finish) are then
+// amortised over 64 KB in both precisions (fp32 was at 70 % of HBM with
+// 32-row tiles and two CTAs per SM).
 template <typename T>
-constexpr int min_blocks() { return sizeof(T) == 4 ? 2 : 1; }
+__host__ __device__ constexpr int rows_per_lane() { return sizeof(T) == 4 ? 2 : 1; }
 
 template <typename T, int CW>
-__global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_kernel(const __grid_constant__ CUtensorMap xmap,
+__global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                                                                       const TmaPassParams p) {
   if (*reinterpret_cast<const volatile int64_t*>(p.done)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int RPL = rows_per_lane<T>();
+  constexpr int KR = kR * RPL;     // tile rows
   constexpr int VB = CW * kWarps;  // tile columns (box width)
-  constexpr uint32_t kTileBytes = kR * VB * sizeof(T);
-  T* xs = reinterpret_cast<T*>(smem_raw);  // [kS][VB][kR] (column-major tile)
+  constexpr uint32_t kTileBytes = KR * VB * sizeof(T);
+  T* xs = reinterpret_cast<T*>(smem_raw);  // [kS][VB][KR] (column-major tile)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kS * kTileBytes);
   uint64_t* empty = full + kS;
   double* dsh = reinterpret_cast<double*>(empty + kS);  // [VB]
-  double* red = dsh + VB;                                // [kWarps][kR]
-  double* es = red + kWarps * kR;                        // [kR]
-  double* ash = es + kR;                                 // [VB] final coefficients (fused residual)
-  double* red2 = ash + VB;                               // [kWarps][kR]
+  double* red = dsh + VB;                                // [kWarps][KR]
+  double* es = red + kWarps * KR;                        // [KR]
+  double* ash = es + KR;                                 // [VB] final coefficients (fused residual)
+  double* red2 = ash + VB;                               // [kWarps][KR]
   const bool want_r = p.afin != nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = static_cast<int>(p.vars);
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
             if (globaltimer() - t0 > kTimeoutNs) return;
         }
         mbar_arrive_expect_tx(&full[s], kTileBytes);
-        tma_2d(xs + static_cast<size_t>(s) * kR * VB, &xmap, static_cast<int>(tile * kR), 0, &full[s]);
+        tma_2d(xs + static_cast<size_t>(s) * KR * VB, &xmap, static_cast<int>(tile * KR), 0, &full[s]);
         if (++s == kS) { s = 0; ph ^= 1u; }
       }
     }
@@ -115,74 +121,94 @@ __global__ void __launch_bounds__(kCons + 32, min_blocks<T>()) gram_pass_tma_ker
   uint32_t ph = 0;
   int prev = -1;
   int64_t tile = blockIdx.x;
-  T e_next = T(0), y_next = T(0);
+  T e_next[RPL], y_next[RPL];
   const T* yv = static_cast<const T*>(p.y);
   T* rv = static_cast<T*>(p.resid);
-  if (warp == 0 && tile < p.ntiles) {
-    const int64_t row = tile * kR + lane;
-    e_next = row < p.obs ? e[row] : T(0);
-    if (want_r) y_next = row < p.obs ? yv[row] : T(0);
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    e_next[i] = T(0);
+    y_next[i] = T(0);
+    if (warp == 0 && tile < p.ntiles) {
+      const int64_t row = tile * KR + lane + 32 * i;
+      e_next[i] = row < p.obs ? e[row] : T(0);
+      if (want_r) y_next[i] = row < p.obs ? yv[row] : T(0);
+    }
   }
   for (; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t row = tile * kR + lane;
-    const T e_cur = e_next, y_cur = y_next;
-    if (warp == 0) {
-      const int64_t nrow = (tile + gridDim.x) * kR + lane;
-      const bool nok = tile + gridDim.x < p.ntiles && nrow < p.obs;
-      e_next = nok ? e[nrow] : T(0);
-      if (want_r) y_next = nok ? yv[nrow] : T(0);
+    T e_cur[RPL], y_cur[RPL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      e_cur[i] = e_next[i];
+      y_cur[i] = y_next[i];
+      if (warp == 0) {
+        const int64_t nrow = (tile + gridDim.x) * KR + lane + 32 * i;
+        const bool nok = tile + gridDim.x < p.ntiles && nrow < p.obs;
+        e_next[i] = nok ? e[nrow] : T(0);
+        if (want_r) y_next[i] = nok ? yv[nrow] : T(0);
+      }
     }
     {
       const uint64_t t0 = globaltimer();
       while (!mbar_test(&full[s], ph))
         if (globaltimer() - t0 > kTimeoutNs) break;
     }
-    const T* X = xs + static_cast<size_t>(s) * kR * VB + static_cast<size_t>(warp) * CW * kR + lane;
+    const T* X = xs + static_cast<size_t>(s) * KR * VB + static_cast<size_t>(warp) * CW * KR + lane;
     if (p.apply) {
-      double t = 0.0;
 #pragma unroll
-      for (int q = 0; q < CW; ++q) t = __fma_rn(static_cast<double>(X[q * kR]), dsh[warp * CW + q], t);
-      red[warp * kR + lane] = t;
+      for (int i = 0; i < RPL; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < CW; ++q) t = __fma_rn(static_cast<double>(X[q * KR + 32 * i]), dsh[warp * CW + q], t);
+        red[warp * KR + lane + 32 * i] = t;
+      }
     }
     if (want_r) {
-      double t2 = 0.0;
 #pragma unroll
-      for (int q = 0; q < CW; ++q) t2 = __fma_rn(static_cast<double>(X[q * kR]), ash[warp * CW + q], t2);
-      red2[warp * kR + lane] = t2;
+      for (int i = 0; i < RPL; ++i) {
+        double t2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < CW; ++q) t2 = __fma_rn(static_cast<double>(X[q * KR + 32 * i]), ash[warp * CW + q], t2);
+        red2[warp * KR + lane + 32 * i] = t2;
+      }
     }
     bar_cons();
     if (tid == 0 && prev >= 0) mbar_arrive1(&empty[prev]);  // previous tile fully consumed
     if (warp == 0) {
-      double ev = static_cast<double>(e_cur);
-      if (p.apply) {
-        double tt = 0.0;
 #pragma unroll
-        for (int c = 0; c < kWarps; ++c) tt += red[c * kR + lane];
-        const T en = static_cast<T>(ev - tt);
-        if (row < p.obs) e[row] = en;
-        ev = static_cast<double>(en);
-        sq = __fma_rn(ev, ev, sq);
-      } else {
-        sq = __fma_rn(ev, ev, sq);  // dot-only pass: sum e^2 of the unchanged e (column scoring)
-      }
-      es[lane] = ev;
-      if (want_r && row < p.obs) {
-        double r2 = 0.0;
+      for (int i = 0; i < RPL; ++i) {
+        const int64_t row = tile * KR + lane + 32 * i;
+        double ev = static_cast<double>(e_cur[i]);
+        if (p.apply) {
+          double tt = 0.0;
 #pragma unroll
-        for (int c = 0; c < kWarps; ++c) r2 += red2[c * kR + lane];
-        rv[row] = static_cast<T>(static_cast<double>(y_cur) - r2);
+          for (int c = 0; c < kWarps; ++c) tt += red[c * KR + lane + 32 * i];
+          const T en = static_cast<T>(ev - tt);
+          if (row < p.obs) e[row] = en;
+          ev = static_cast<double>(en);
+        }
+        sq = __fma_rn(ev, ev, sq);  // (dot-only pass: sum e^2 of the unchanged e, for column scoring)
+        es[lane + 32 * i] = ev;
+        if (want_r && row < p.obs) {
+          double r2 = 0.0;
+#pragma unroll
+          for (int c = 0; c < kWarps; ++c) r2 += red2[c * KR + lane + 32 * i];
+          rv[row] = static_cast<T>(static_cast<double>(y_cur[i]) - r2);
+        }
       }
     }
     bar_cons();
     if (p.dot) {
-      const double er = es[lane];
 #pragma unroll
-      for (int q = 0; q < CW; ++q) acc[q] = __fma_rn(static_cast<double>(X[q * kR]), er, acc[q]);
+      for (int i = 0; i < RPL; ++i) {
+        const double er = es[lane + 32 * i];
+#pragma unroll
+        for (int q = 0; q < CW; ++q) acc[q] = __fma_rn(static_cast<double>(X[q * KR + 32 * i]), er, acc[q]);
+      }
     }
     prev = s;
     if (++s == kS) { s = 0; ph ^= 1u; }
   }
-  // column partials: sum over the 32 tile rows (lanes), fixed butterfly order
+  // column partials: sum over the tile rows (lanes), fixed butterfly order
   if (p.dot) {
 #pragma unroll
     for (int q = 0; q < CW; ++q) {
@@ -214,8 +240,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <typename T, int CW>
 int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStream_t st) {
   constexpr int VB = CW * kWarps;
-  const size_t smem = kS * static_cast<size_t>(kR) * VB * sizeof(T) + 2 * kS * 8 + 2 * VB * 8 + 2 * kWarps * kR * 8 +
-                      kR * 8;
+  constexpr int KR = kR * rows_per_lane<T>();
+  const size_t smem = kS * static_cast<size_t>(KR) * VB * sizeof(T) + 2 * kS * 8 + 2 * VB * 8 + 2 * kWarps * KR * 8 +
+                      KR * 8;
   auto kern = gram_pass_tma_kernel<T, CW>;
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<grid, kCons + 32, smem, st>>>(map, p);
@@ -228,7 +255,10 @@ int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStre
 
 bool gram_tma_supported(int64_t vars) { return vars >= 1 && vars <= 256 && encode_fn() != nullptr; }
 
-int gram_tma_grid(int dtype) { return (dtype == BAK_F32 ? 2 : 1) * device_sms(); }
+int gram_tma_grid(int dtype) {
+  (void)dtype;
+  return device_sms();  // one CTA per SM, 64 KB tiles in both precisions
+}
 
 // x: column-major obs x vars, ldx*sizeof(T) % 16 == 0
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
@@ -245,7 +275,8 @@ int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int
   CUtensorMap map;
   cuuint64_t gdim[2] = {static_cast<cuuint64_t>(obs), static_cast<cuuint64_t>(vars)};
   cuuint64_t gstr[1] = {static_cast<cuuint64_t>(ldx * ts)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kR), static_cast<cuuint32_t>(vb)};
+  const int kr = kR * (dtype == BAK_F64 ? 1 : 2);  // tile rows (rows_per_lane)
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kr), static_cast<cuuint32_t>(vb)};
   cuuint32_t est[2] = {1, 1};
   CUresult r = enc(&map, dtype == BAK_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                    const_cast<void*>(x), gdim, gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -254,7 +285,7 @@ int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int
     set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
     return BAK_ECUDA;
   }
-  TmaPassParams p{obs, vars, (obs + kR - 1) / kR, e, delta, apply, dot, gpart, sqpart, done, afin, y, resid};
+  TmaPassParams p{obs, vars, (obs + kr - 1) / kr, e, delta, apply, dot, gpart, sqpart, done, afin, y, resid};
   const int grid = gram_tma_grid(dtype);
   if (dtype == BAK_F64) {
     if (cw == 8) return launch_cw<double, 8>(map, p, grid, st);

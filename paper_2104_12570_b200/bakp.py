@@ -28,8 +28,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .bak import (DRIFT_TOL, SolveConfig, SolveReport, _ptr, _residual, _stream_ptr, _sumsq, _to_device_vector,
-                  _torch, _workspace_bytes, _Workspace, colnorms, solve_bak, to_device_matrix)
+from .bak import (_host, DRIFT_TOL, SolveConfig, SolveReport, _ptr, _residual, _stream_ptr, _sumsq,
+                  _to_device_vector, _torch, _workspace_bytes, _Workspace, colnorms, solve_bak, to_device_matrix)
 
 DIVERGENCE_FACTOR = 10.0              # bakp.py:32
 _BLOCK_VARIANTS = ("auto", "cta", "cluster", "stream", "gram")
@@ -191,7 +191,7 @@ def solve_bakp(x, y, config: BlockConfig | None = None, *, variant="auto", devic
     wall = time.perf_counter() - t0
     return SolveReport(
         a_hat=a if return_device else a.cpu().numpy(),
-        residual=resid if return_device else resid.cpu().numpy(),
+        residual=resid if return_device else _host(resid),
         residual_norm_history=hist[:sweeps].cpu().tolist() if base.record_history else None,
         sweeps_run=sweeps, converged=converged, wall_time=wall,
         drift_warning=bool(drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny) > DRIFT_TOL),

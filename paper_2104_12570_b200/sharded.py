@@ -25,7 +25,7 @@ import time
 import numpy as np
 
 from . import _lib
-from .bak import (DRIFT_TOL, DeviceMatrix, SolveConfig, SolveReport, _permutation_chunks, _ptr, _stream_ptr,
+from .bak import (_host, DRIFT_TOL, DeviceMatrix, SolveConfig, SolveReport, _permutation_chunks, _ptr, _stream_ptr,
                   _to_device_vector, _torch, _Workspace, colnorms, to_device_matrix)
 
 
@@ -282,7 +282,7 @@ def _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return
     drift_warn = bool(drift / max(np.sqrt(ynorm2), np.finfo(np.float64).tiny) > DRIFT_TOL)
     history = hist[:sweeps].cpu().tolist() if hist is not None else None
     a_out = a if return_device else a.cpu().numpy()
-    return [SolveReport(a_hat=a_out, residual=r if return_device else r.cpu().numpy(), residual_norm_history=history,
+    return [SolveReport(a_hat=a_out, residual=r if return_device else _host(r), residual_norm_history=history,
                         sweeps_run=sweeps, converged=converged, wall_time=wall, drift_warning=drift_warn,
                         variant=label) for r in resids]
 

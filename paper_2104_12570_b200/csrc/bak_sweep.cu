@@ -47,7 +47,8 @@
 namespace bak {
 namespace {
 
-constexpr int kModeCta = 0, kModeCluster = 1, kModeGrid = 2;
+constexpr int kModeCta = 0, kModeCluster = 1, kModeGrid = 2, kModeGridCl = 3;
+constexpr int kGridCluster = 8;  // CTAs per cluster in kModeGridCl (portable size)
 constexpr int kMaxCluster = 16;
 constexpr int kMaxStages = 16;
 constexpr int kMaxConsumers = 256;
@@ -118,12 +119,18 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   const int S = prm.nstages;
 
   uint32_t rank = 0, G = 1;
+  uint32_t crank = 0, C = 1;  // kModeGridCl: rank within the cluster, cluster size
   if (MODE == kModeCluster) {
     rank = cluster_rank();
     G = cluster_size();
   } else if (MODE == kModeGrid) {
     rank = blockIdx.x;
     G = gridDim.x;
+  } else if (MODE == kModeGridCl) {
+    rank = blockIdx.x;
+    G = gridDim.x;
+    crank = cluster_rank();
+    C = cluster_size();
   }
 
   const T* __restrict__ x = static_cast<const T*>(prm.x);
@@ -153,6 +160,8 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   off += 2 * 8;
   Pair* bcast = reinterpret_cast<Pair*>(smem_raw + off);  // [2]
   off += 2 * sizeof(Pair);
+  uint64_t* xbar2 = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2] kModeGridCl broadcast
+  off += 2 * 8;
   volatile int* stop = reinterpret_cast<volatile int*>(smem_raw + off);
 
   if (tid == 0) {
@@ -162,11 +171,13 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     }
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
+    mbar_init(&xbar2[0], 1);
+    mbar_init(&xbar2[1], 1);
     *stop = 0;
     fence_mbar_init();
   }
   __syncthreads();
-  if (MODE == kModeCluster) cluster_sync();
+  if (MODE == kModeCluster || MODE == kModeGridCl) cluster_sync();
 
   const int64_t ncols = prm.ncols;
   const int64_t total = prm.max_iter * ncols;
@@ -362,6 +373,80 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         Q = sq[0];
         return false;
       }
+      if (MODE == kModeGridCl) {
+        // (1) cluster: every CTA st.async's its partial into every peer's slot
+        //     (DSMEM, completes as tx bytes on the peer's mbarrier) -> every CTA
+        //     sums the cluster's C partials in rank order;
+        // (2) grid: each cluster leader posts the cluster sum as an epoch-tagged
+        //     record, gathers the ncl records (one per lane, <= 32 clusters) and
+        //     sums them with a fixed butterfly -> identical bits in every leader;
+        // (3) the leader st.async's the total into every peer of its cluster.
+        const uint32_t par = (rc >> 1) & 1;
+        if (tid < static_cast<int>(C)) {
+          const uint32_t rs = mapa(smem_addr(&xslot[buf * kMaxCluster + crank]), tid);
+          const uint32_t rb = mapa(smem_addr(&xbar[buf]), tid);
+          st_async_v2(rs, static_cast<double>(bp), static_cast<double>(bq), rb);
+        }
+        if (tid == 0) {
+          mbar_arrive_expect_tx(&xbar[buf], C * 16u);
+          mbar_arrive_expect_tx(&xbar2[buf], 16u);
+        }
+        bool timed_out = false;
+        if (crank == 0 && warp == 0) {
+          if (!mbar_test_cluster(&xbar[buf], par)) {
+            const uint64_t t0 = globaltimer();
+            while (!mbar_test_cluster(&xbar[buf], par))
+              if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+          }
+          T cp = T(0), cq = T(0);
+          for (uint32_t r = 0; r < C; ++r) {
+            cp = Num<T>::add(cp, static_cast<T>(xslot[buf * kMaxCluster + r].p));
+            if (with_q) cq = Num<T>::add(cq, static_cast<T>(xslot[buf * kMaxCluster + r].q));
+          }
+          const uint32_t epoch = rc + 1;
+          uint32_t* part = prm.slots + static_cast<size_t>(buf) * kGridSlotsMax * 8;
+          const uint32_t cid = blockIdx.x / C, ncl = gridDim.x / C;
+          if (lane == 0) {
+            ll_store(part + static_cast<size_t>(cid) * 8, static_cast<double>(cp), epoch);
+            if (with_q) ll_store(part + static_cast<size_t>(cid) * 8 + 4, static_cast<double>(cq), epoch);
+          }
+          T vp = T(0), vq = T(0);
+          if (lane < static_cast<int>(ncl)) {
+            double v = 0.0;
+            const uint64_t t0 = globaltimer();
+            while (!ll_load(part + static_cast<size_t>(lane) * 8, epoch, v))
+              if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+            vp = static_cast<T>(v);
+            if (with_q) {
+              while (!ll_load(part + static_cast<size_t>(lane) * 8 + 4, epoch, v))
+                if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+              vq = static_cast<T>(v);
+            }
+          }
+          const T sp = warp_sum(vp);
+          const T sq = with_q ? warp_sum(vq) : T(0);
+          if (lane < static_cast<int>(C)) {
+            const uint32_t rs = mapa(smem_addr(&bcast[buf]), lane);
+            const uint32_t rb = mapa(smem_addr(&xbar2[buf]), lane);
+            st_async_v2(rs, static_cast<double>(sp), static_cast<double>(sq), rb);
+          }
+        }
+        if (warp == 0) {
+          if (!mbar_test_cluster(&xbar2[buf], par)) {
+            const uint64_t t0 = globaltimer();
+            while (!mbar_test_cluster(&xbar2[buf], par))
+              if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+          }
+          if (timed_out) {
+            report_error(prm.status, BAK_ETIMEOUT);
+            my_abort = 1;
+          }
+        }
+        const bool any2 = bar_or(NT, my_abort);
+        P = static_cast<T>(bcast[buf].p);
+        Q = static_cast<T>(bcast[buf].q);
+        return any2;
+      }
       // kModeGrid: partial records -> aggregator (CTA 0) -> per-CTA result lines
       const uint32_t epoch = rc + 1;
       uint32_t* part = prm.slots + static_cast<size_t>(buf) * kGridSlotsMax * 8;
@@ -547,14 +632,14 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     }
   }
   __syncthreads();
-  if (MODE == kModeCluster) cluster_sync();
+  if (MODE == kModeCluster || MODE == kModeGridCl) cluster_sync();
 }
 
 // ------------------------------- host -------------------------------------
 
 size_t smem_bytes(const SweepPlan& pl, size_t tsize) {
   return static_cast<size_t>(pl.nstages) * pl.stage_elems * tsize + 2 * kMaxStages * 8 +
-         kMaxStages * sizeof(StageMeta) + 2 * 2 * 32 * tsize + 16 + 2 * kMaxCluster * 16 + 16 + 32 + 16;
+         kMaxStages * sizeof(StageMeta) + 2 * 2 * 32 * tsize + 16 + 2 * kMaxCluster * 16 + 16 + 32 + 16 + 16;
 }
 
 template <typename T, int E, int MODE, int MAXNT>
@@ -567,7 +652,7 @@ int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
   cfg.blockDim = dim3(pl.nthreads + 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   int na = 0;
   if (MODE == kModeCluster) {
     if (pl.nparticipants > 8)
@@ -581,9 +666,28 @@ int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
     ++na;
+  } else if (MODE == kModeGridCl) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = kGridCluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  if (MODE == kModeGridCl) {
+    // every cluster must be co-resident (spin waits across clusters)
+    int ncl = 0;
+    BAK_CHECK_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg));
+    if (ncl < pl.nparticipants / kGridCluster) {
+      set_error("bak_sweep(GRID): %d clusters of %d do not fit co-resident (max %d)", pl.nparticipants / kGridCluster,
+                kGridCluster, ncl);
+      return BAK_EUNSUPPORTED;
+    }
+  }
   BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   count_launches(1);
   return BAK_OK;
@@ -607,6 +711,38 @@ template <typename T, int MODE>
 int launch_nt(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   if (pl.nthreads == 32) return launch_e<T, MODE, 32>(pl, prm, st);
   return launch_e<T, MODE, kMaxConsumers>(pl, prm, st);
+}
+
+// How many clusters of kGridCluster CTAs of the sweep kernel (one CTA per SM:
+// its ring fills the shared memory) can be co-resident — GPC boundaries make
+// it less than SMs / kGridCluster (B200: 15 clusters of 8 = 120 CTAs).
+int grid_cluster_capacity() {
+  static int cap = -1;
+  if (cap >= 0) return cap;
+  auto kern = sweep_kernel<double, 8, kModeGridCl, kMaxConsumers>;
+  const int smem = device_max_smem_optin() - 2048;
+  cap = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return cap;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kGridCluster * 8);
+  cfg.blockDim = dim3(kMaxConsumers + 32);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = kGridCluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess) cap = n;
+  else cudaGetLastError();
+  return cap;
 }
 
 }  // namespace
@@ -679,6 +815,28 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
     return false;
   }
   if (variant == BAK_VARIANT_GRID) {
+    // two-level exchange: clusters of kGridCluster CTAs reduce through DSMEM,
+    // cluster leaders through global records (<= 32 clusters); rows spread
+    // evenly over a multiple of kGridCluster CTAs.  BAK_GRID_FLAT=1: one level.
+    const char* flat = getenv("BAK_GRID_FLAT");
+    const int max_parts = kGridCluster * (grid_cluster_capacity() < 32 ? grid_cluster_capacity() : 32);
+    if (!(flat && flat[0] == '1')) {
+      for (int e : kEs) {
+        const int64_t rows = 256LL * e;
+        const int64_t parts = round_up((obs + rows - 1) / rows, kGridCluster);
+        if (parts > sms || parts > max_parts) continue;
+        const int64_t rpc = round_up((obs + parts - 1) / parts, 4);
+        if ((parts - 1) * rpc >= obs) continue;
+        SweepPlan cand;
+        if (!plan_fill(dtype, variant, obs, 256, e, static_cast<int>((obs + rows - 1) / rows), cand, 3)) continue;
+        cand.nparticipants = static_cast<int>(parts);
+        cand.rows_per_cta = rpc;
+        cand.stage_elems = rpc;
+        cand.cluster = kGridCluster;
+        pl = cand;
+        return true;
+      }
+    }
     for (int nt : {256}) {
       for (int e : kEs) {
         const int64_t rows = static_cast<int64_t>(nt) * e;
@@ -694,6 +852,24 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
 int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   if (pl.variant == BAK_VARIANT_GRID && prm.slots)
     BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, kGridSlotBytes, st));
+  if (pl.variant == BAK_VARIANT_GRID && pl.cluster) {
+    const int rc = dtype == BAK_F64 ? launch_nt<double, kModeGridCl>(pl, prm, st)
+                                    : launch_nt<float, kModeGridCl>(pl, prm, st);
+    if (rc != BAK_EUNSUPPORTED) return rc;
+    // clusters did not fit co-resident: one-level grid exchange
+    if (getenv("BAK_DEBUG")) fprintf(stderr, "bak: two-level grid exchange unavailable (%s)\n", bak_last_error());
+    SweepPlan flat;
+    setenv("BAK_GRID_FLAT", "1", 0);
+    const bool ok = plan_onchip(dtype, BAK_VARIANT_GRID, prm.obs, flat);
+    unsetenv("BAK_GRID_FLAT");
+    if (!ok) return rc;
+    g_err_clear();
+    SweepParams p2 = prm;
+    p2.rows_per_cta = flat.rows_per_cta;
+    p2.stage_elems = flat.stage_elems;
+    p2.nstages = flat.nstages;
+    return dtype == BAK_F64 ? launch_nt<double, kModeGrid>(flat, p2, st) : launch_nt<float, kModeGrid>(flat, p2, st);
+  }
   if (dtype == BAK_F64) {
     if (pl.variant == BAK_VARIANT_CTA) return launch_nt<double, kModeCta>(pl, prm, st);
     if (pl.variant == BAK_VARIANT_CLUSTER) return launch_nt<double, kModeCluster>(pl, prm, st);

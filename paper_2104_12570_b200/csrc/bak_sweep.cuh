@@ -37,6 +37,7 @@ struct SweepPlan {
   int nstages = 2;
   int64_t rows_per_cta = 0;
   int64_t stage_elems = 0;
+  int cluster = 0;  // GRID: CTAs per cluster of the two-level exchange (0 = one level)
 };
 
 bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl);

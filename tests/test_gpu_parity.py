@@ -359,3 +359,24 @@ def test_gram_pipelined_host_upload_matches_oracle(precision, monkeypatch):
     rep2 = pb.solve_bak(hx, y, pb.SolveConfig(max_iter=80, tol=1e-6), variant="gram")
     ref2 = orc.solve(x, y, max_iter=80, tol=1e-6)
     assert rep2.sweeps_run == ref2["sweeps_run"] and rep2.converged == ref2["converged"]
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_grid_two_level_and_flat_exchange_match_oracle(precision, monkeypatch):
+    """GRID variant: the two-level exchange (clusters of 8 through DSMEM, then
+    cluster leaders through global records) and the one-level aggregator both
+    meet the bar, and each is deterministic run to run."""
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=200_000, nvars=16, precision=precision)
+    ref = orc.solve(x, y, max_iter=4, tol=0, record_history=True)
+    tol = TOL[np.dtype(x.dtype)]
+    outs = {}
+    for flat in ("0", "1"):
+        monkeypatch.setenv("BAK_GRID_FLAT", flat)
+        r1 = pb.solve_bak(x, y, pb.SolveConfig(max_iter=4, tol=0, record_history=True), variant="grid")
+        r2 = pb.solve_bak(x, y, pb.SolveConfig(max_iter=4, tol=0, record_history=True), variant="grid")
+        assert r1.variant == "grid" and r1.a_hat.tobytes() == r2.a_hat.tobytes()
+        assert orc.rel_coeff_err(r1.a_hat, ref["a_hat"]) <= tol
+        np.testing.assert_allclose(r1.residual_norm_history, ref["residual_norm_history"], rtol=max(1e3 * tol, 1e-6))
+        outs[flat] = r1.a_hat
+    assert orc.rel_coeff_err(outs["0"], outs["1"]) <= tol

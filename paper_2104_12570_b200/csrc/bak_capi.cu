@@ -51,6 +51,11 @@ int device_max_smem_optin() {
   return cached_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448, cache);
 }
 
+int64_t l2_bytes() {
+  static int cache[64] = {0};
+  return cached_attr(cudaDevAttrL2CacheSize, 126 << 20, cache);
+}
+
 }  // namespace bak
 
 using namespace bak;

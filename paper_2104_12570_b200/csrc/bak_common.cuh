@@ -205,6 +205,7 @@ inline size_t dtype_size(int dtype) { return dtype == BAK_F64 ? 8 : 4; }
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 int device_sms();
 int device_max_smem_optin();
+int64_t l2_bytes();
 void count_launches(int n);
 }  // namespace bak
 

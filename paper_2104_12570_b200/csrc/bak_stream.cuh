@@ -38,10 +38,13 @@ struct StreamCursor {
 
 constexpr int kUnroll = 4;
 
+// keep_next: load x_{j+1} with the normal L2 policy (it is x_j of the next
+// column step, re-read from L2 when e + one column fit in L2) and x_j with the
+// evict-first hint (its last use); otherwise both evict-first.
 template <typename T>
 __device__ __forceinline__ void stream_pass(T* __restrict__ e, const T* __restrict__ xc, const T* __restrict__ xn,
                                             int64_t nrows, T d, bool upd, bool dot, bool sq, bool backward, T& p,
-                                            T& q) {
+                                            T& q, bool keep_next = false) {
   using VT = Vec16<T>;
   using V = typename VT::V;
   const int NT = blockDim.x, tid = threadIdx.x;
@@ -64,7 +67,7 @@ __device__ __forceinline__ void stream_pass(T* __restrict__ e, const T* __restri
     for (int u = 0; u < kUnroll; ++u) {
       E[u] = ev[idx[u]];
       if (upd) XC[u] = __ldcs(xcv + idx[u]);
-      if (dot) XN[u] = __ldcs(xnv + idx[u]);
+      if (dot) XN[u] = keep_next ? __ldcg(xnv + idx[u]) : __ldcs(xnv + idx[u]);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -91,7 +94,7 @@ __device__ __forceinline__ void stream_pass(T* __restrict__ e, const T* __restri
     V E1 = ev[i];
     V XC1, XN1;
     if (upd) XC1 = __ldcs(xcv + i);
-    if (dot) XN1 = __ldcs(xnv + i);
+    if (dot) XN1 = keep_next ? __ldcg(xnv + i) : __ldcs(xnv + i);
 #pragma unroll
     for (int c = 0; c < VT::N; ++c) {
       T ee = VT::get(E1, c);

@@ -27,6 +27,7 @@ struct SweepParams {
   int64_t rows_per_cta;
   int64_t stage_elems;
   int nstages;
+  int keep_next;  // STREAM: keep x_{j+1} in L2 for the next column step
 };
 
 struct SweepPlan {

@@ -19,6 +19,8 @@
 // of a (a + r*vars), status (status + 4*r) and history (history + r*max_iter);
 // its mailbox is mailboxes[r].  No CTA ever waits on a kernel that is not
 // co-resident (cooperative launch).
+#include <cstdlib>
+
 #include "bak_common.cuh"
 #include "bak_stream.cuh"
 #include "bak_sweep.cuh"
@@ -42,7 +44,8 @@ struct RowshardParams {
   double thresh2;
   double* history;
   int64_t* status;
-  uint32_t* slots;  // per launch-rank local records: [nr_local][2 bufs][ctas_per_rank][8 u32]
+  uint32_t* slots;  // per launch-rank local records: [nr_local][slot_stride u32]
+  int64_t slot_stride;
   int rank0;        // global rank of launch-rank 0
   int nranks;       // global number of ranks
   int nranks_local;
@@ -50,11 +53,22 @@ struct RowshardParams {
   uint32_t* mbox[kMaxRanks];  // mailbox of every global rank: [2 bufs][nranks][8 u32]
 };
 
-template <typename T>
+constexpr int kRsCluster = 8;
+
+template <typename T, bool CL>
 __global__ void __launch_bounds__(512, 1) rowshard_kernel(const RowshardParams p) {
   __shared__ T red[2 * 2 * 32];
   __shared__ double bc[2][2];
+  __shared__ ClExchange clx;  // two-level exchange state (CL)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t crank = 0, C = 1;
+  if (CL) {
+    crank = cluster_rank();
+    C = cluster_size();
+    cl_exchange_init(clx);
+    __syncthreads();
+    cluster_sync();
+  }
   const int lr = blockIdx.x / p.ctas_per_rank;        // launch-local rank
   const int cta = blockIdx.x % p.ctas_per_rank;      // CTA within the rank
   const uint32_t G = static_cast<uint32_t>(p.ctas_per_rank);
@@ -70,7 +84,7 @@ __global__ void __launch_bounds__(512, 1) rowshard_kernel(const RowshardParams p
   T* __restrict__ ag = static_cast<T*>(p.a) + static_cast<int64_t>(lr) * p.vars;
   int64_t* status = p.status ? p.status + 4 * lr : nullptr;
   double* history = p.history ? p.history + static_cast<int64_t>(lr) * p.max_iter : nullptr;
-  uint32_t* slots = p.slots + static_cast<size_t>(lr) * 2 * G * 8;
+  uint32_t* slots = p.slots + static_cast<size_t>(lr) * p.slot_stride;
   uint32_t* mine = p.mbox[grank];
   const int64_t ncols = p.vars, total = p.max_iter * ncols;
   int my_abort = 0;
@@ -79,6 +93,46 @@ __global__ void __launch_bounds__(512, 1) rowshard_kernel(const RowshardParams p
     const int buf = rc & 1;
     if (block_sum2(pv, qv, with_q, buf, red, my_abort)) return true;
     const uint32_t epoch = p.epoch_base + rc + 1;
+    if (CL) {
+      // clusters of this rank -> rank total (cl_grid_sum), then the cross-rank
+      // stage inside the leaders: cluster 0's leader posts the rank total into
+      // every rank's mailbox, every leader sums the N totals in rank order
+      const uint32_t cid = static_cast<uint32_t>(cta) / C, ncl = G / C;
+      bool to = false;
+      auto hook = [&](T& sp, T& sq, bool& tout) {
+        if (cid == 0 && lane < N) {
+          uint32_t* dst = p.mbox[lane] + (static_cast<size_t>(buf) * N + grank) * 8;
+          ll_store_sys(dst, static_cast<double>(sp), epoch);
+          ll_store_sys(dst + 4, static_cast<double>(sq), epoch);
+        }
+        double vp = 0.0, vq = 0.0;
+        if (lane < N) {
+          const uint32_t* src = mine + (static_cast<size_t>(buf) * N + lane) * 8;
+          const uint64_t t0 = globaltimer();
+          while (!ll_load_sys(src, epoch, vp))
+            if (globaltimer() - t0 > kTimeoutNs) { tout = true; break; }
+          if (with_q)
+            while (!ll_load_sys(src + 4, epoch, vq))
+              if (globaltimer() - t0 > kTimeoutNs) { tout = true; break; }
+        }
+        T tp = T(0), tq = T(0);
+        for (int r = 0; r < N; ++r) {
+          tp = Num<T>::add(tp, static_cast<T>(__shfl_sync(0xffffffffu, vp, r)));
+          if (with_q) tq = Num<T>::add(tq, static_cast<T>(__shfl_sync(0xffffffffu, vq, r)));
+        }
+        sp = tp;
+        sq = tq;
+      };
+      cl_grid_sum<T>(clx, pv, qv, with_q, rc, slots, epoch, crank, C, cid, ncl, to, hook);
+      if (to) {
+        report_error(status, BAK_ETIMEOUT);
+        my_abort = 1;
+      }
+      const bool ab = __syncthreads_or(my_abort) != 0;
+      P = static_cast<T>(clx.bcast[buf].p);
+      Q = static_cast<T>(clx.bcast[buf].q);
+      return ab;
+    }
     uint32_t* ls = slots + static_cast<size_t>(buf) * G * 8;
     if (tid == 0) {
       ll_store(ls + static_cast<size_t>(cta) * 8, static_cast<double>(pv), epoch);
@@ -174,6 +228,32 @@ __global__ void __launch_bounds__(512, 1) rowshard_kernel(const RowshardParams p
     status[3] = BAK_VARIANT_STREAM;
   }
   (void)total;
+  if (CL) {
+    __syncthreads();
+    cluster_sync();
+  }
+}
+
+template <typename T>
+int rowshard_cluster_capacity() {
+  static int cap = -1;
+  if (cap >= 0) return cap;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kRsCluster * 4);
+  cfg.blockDim = dim3(512);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = kRsCluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  int n = 0;
+  cap = cudaOccupancyMaxActiveClusters(&n, rowshard_kernel<T, true>, &cfg) == cudaSuccess ? n : 0;
+  cudaGetLastError();
+  return cap;
 }
 
 }  // namespace
@@ -203,10 +283,20 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
     return BAK_EINVAL;
   }
   const int sms = device_sms();
-  const int per_rank_ctas = imax64(1, sms / nranks_local);
+  int per_rank_ctas = imax64(1, sms / nranks_local);
+  // two-level exchange: whole clusters of 8 per rank (<= 32 per rank), all co-resident
+  const char* flat = getenv("BAK_STREAM_FLAT");
+  const int cap = dtype == BAK_F64 ? rowshard_cluster_capacity<double>() : rowshard_cluster_capacity<float>();
+  int cl_per_rank = static_cast<int>(imin64(imin64(cap, sms / kRsCluster) / nranks_local, 32));
+  // (only when it keeps >= 3/4 of the CTAs: with many emulated ranks per GPU
+  // one cluster per rank would starve the streaming passes of bandwidth)
+  const bool use_cl = !(flat && flat[0] == '1') && cl_per_rank >= 1 &&
+                      4 * cl_per_rank * kRsCluster >= 3 * per_rank_ctas;
+  if (use_cl) per_rank_ctas = cl_per_rank * kRsCluster;
   const int64_t rows_per_rank = round_up((obs_local + nranks_local - 1) / nranks_local, vec);
   const int64_t rows_per_cta = round_up((rows_per_rank + per_rank_ctas - 1) / per_rank_ctas, vec);
-  const int64_t need = static_cast<int64_t>(nranks_local) * 2 * per_rank_ctas * 32;
+  const int64_t slot_stride = imax64(2LL * per_rank_ctas * 8, 2LL * 32 * 8);  // u32 per launch-rank
+  const int64_t need = static_cast<int64_t>(nranks_local) * slot_stride * 4;
   if (!workspace || workspace_bytes < need) {
     set_error("bak_sweep_rowshard: workspace too small (need %lld)", (long long)need);
     return BAK_EWORKSPACE;
@@ -228,6 +318,7 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
   p.history = history;
   p.status = status;
   p.slots = static_cast<uint32_t*>(workspace);
+  p.slot_stride = slot_stride;
   p.rank0 = rank;
   p.nranks = nranks;
   p.nranks_local = nranks_local;
@@ -239,15 +330,19 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
   cfg.gridDim = dim3(per_rank_ctas * nranks_local);
   cfg.blockDim = dim3(512);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = kRsCluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = use_cl ? 2 : 1;
   if (dtype == BAK_F64)
-    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, rowshard_kernel<double>, p));
+    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, use_cl ? rowshard_kernel<double, true> : rowshard_kernel<double, false>, p));
   else
-    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, rowshard_kernel<float>, p));
+    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, use_cl ? rowshard_kernel<float, true> : rowshard_kernel<float, false>, p));
   count_launches(1);
   return BAK_OK;
 }

@@ -355,7 +355,7 @@ def sweep_rowshard(dm, e, a, norms, max_iter, thresh2, mailboxes, rank, nranks, 
     dev = dm.data.device
     st = stream if stream is not None else _stream_ptr(torch, dev)
     ctas = max(1, (lib.bak_device_sm_count() or 148) // nranks_local)
-    ws = _Workspace(torch, dev, nranks_local * 2 * ctas * 32 + 4096)
+    ws = _Workspace(torch, dev, nranks_local * max(2 * ctas * 32, 2048) + 4096)
     if status is None:
         status = torch.zeros(4 * nranks_local, dtype=torch.int64, device=dev)
     base = mailboxes.next_epochs(max_iter * dm.vars + 1)

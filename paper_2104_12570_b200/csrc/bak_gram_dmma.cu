@@ -5,10 +5,9 @@
 // Only the lower block triangle of 64x64 blocks is computed (bi >= bj), split
 // over K (rows of x) into chunks; a CTA = 4 warps owns one (block, chunk) and
 // each warp a 32x32 quarter = 4x4 DMMA tiles.  Panels of 32 rows x 64 columns
-// stream through a 2-stage cp.async ring (zero-filled past obs / vars), 3 CTAs
-// per SM in one wave; panel layout is column-major with a 36-element column
-// stride so that the m8n8k4 fragment loads (8 columns x 4 rows per warp) are
-// bank-conflict free.  Partials per chunk are summed in chunk order
+// stream through a 2-stage cp.async ring (16-row stages, zero-filled past obs /
+// vars), 4 CTAs per SM in one wave; panel layout is column-major with a
+// (stage rows + 4)-element column stride for the m8n8k4 fragment loads.  Partials per chunk are summed in chunk order
 // (deterministic) and mirrored.  Diagonal-block CTAs optionally also produce
 // the first sweep's g = X^T e (warp 1, whose quarter of a diagonal block is
 // unused), so the solve skips its first pass over x.
@@ -59,11 +58,12 @@ __device__ __forceinline__ void tri_index_strict(int o, int& bi, int& bj) {
   bj = o - bi * (bi - 1) / 2;
 }
 
-template <typename T, int kStages, int kMinBlocks>
+template <typename T, int kStages, int kMinBlocks, int KT = kKT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const GramParams p) {
+  constexpr int kLdT = KT + 4;  // smem column stride (elements)
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* pa = reinterpret_cast<T*>(smem_raw);                  // [stages][64][kLd]
-  T* pb = pa + static_cast<size_t>(kStages) * kBT * kLd;  // [stages][64][kLd] (diagonal CTAs: e panel)
+  T* pa = reinterpret_cast<T*>(smem_raw);                  // [stages][64][kLdT]
+  T* pb = pa + static_cast<size_t>(kStages) * kBT * kLdT;  // [stages][64][kLdT] (diagonal CTAs: e panel)
   // Load balance: a diagonal block needs 3 of the 4 warp quarters, so its CTAs
   // take 4/3 as many rows (cd ~ 3/4 co).  Diagonal CTAs come first.
   const int ndc = p.nb * p.cd;
@@ -88,13 +88,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
   const bool with_e = diag && ev != nullptr;
   const int64_t k_begin = static_cast<int64_t>(chk) * chunk;
   const int64_t k_end = imin64(p.obs, k_begin + chunk);
-  const int nsteps = k_end > k_begin ? static_cast<int>((k_end - k_begin + kKT - 1) / kKT) : 0;
+  const int nsteps = k_end > k_begin ? static_cast<int>((k_end - k_begin + KT - 1) / KT) : 0;
   constexpr int kPer = 16 / sizeof(T);               // elements per 16-byte piece
-  constexpr int kPieces = kKT / kPer;                // pieces per column per stage
+  constexpr int kPieces = KT / kPer;                // pieces per column per stage
   constexpr int kCopies = kBT * kPieces / kThreads;  // per thread per panel
 
   auto load_stage = [&](int step, int slot) {
-    const int64_t k0 = k_begin + static_cast<int64_t>(step) * kKT;
+    const int64_t k0 = k_begin + static_cast<int64_t>(step) * KT;
 #pragma unroll
     for (int i = 0; i < kCopies; ++i) {
       const int id = tid + i * kThreads;
@@ -105,20 +105,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
         const int64_t gc = static_cast<int64_t>(bi) * kBT + col;
         const int bytes = (gc < p.vars && rem > 0) ? static_cast<int>(imin64(rem, kPer) * sizeof(T)) : 0;
         const T* src = bytes ? x + gc * p.ldx + row : x;
-        cp_async16(pa + (static_cast<size_t>(slot) * kBT + col) * kLd + piece * kPer, src, bytes);
+        cp_async16(pa + (static_cast<size_t>(slot) * kBT + col) * kLdT + piece * kPer, src, bytes);
       }
       if (!diag) {
         const int64_t gc = static_cast<int64_t>(bj) * kBT + col;
         const int bytes = (gc < p.vars && rem > 0) ? static_cast<int>(imin64(rem, kPer) * sizeof(T)) : 0;
         const T* src = bytes ? x + gc * p.ldx + row : x;
-        cp_async16(pb + (static_cast<size_t>(slot) * kBT + col) * kLd + piece * kPer, src, bytes);
+        cp_async16(pb + (static_cast<size_t>(slot) * kBT + col) * kLdT + piece * kPer, src, bytes);
       }
     }
     if (with_e && tid < kPieces) {  // the residual rows of this stage (diagonal CTAs only)
       const int64_t row = k0 + tid * kPer;
       const int64_t rem = k_end - row;
       const int bytes = rem > 0 ? static_cast<int>(imin64(rem, kPer) * sizeof(T)) : 0;
-      cp_async16(pb + static_cast<size_t>(slot) * kBT * kLd + tid * kPer, bytes ? ev + row : ev, bytes);
+      cp_async16(pb + static_cast<size_t>(slot) * kBT * kLdT + tid * kPer, bytes ? ev + row : ev, bytes);
     }
   };
   // fused g0 (warp 1 of a diagonal CTA owns the unused upper quadrant: no DMMA work)
@@ -145,15 +145,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
       cp_async_commit();
     }
     const int slot = step % kStages;
-    const T* A = pa + static_cast<size_t>(slot) * kBT * kLd;
-    const T* B = diag ? A : pb + static_cast<size_t>(slot) * kBT * kLd;
+    const T* A = pa + static_cast<size_t>(slot) * kBT * kLdT;
+    const T* B = diag ? A : pb + static_cast<size_t>(slot) * kBT * kLdT;
 #pragma unroll
-    for (int k4 = 0; k4 < kKT; k4 += 4) {
+    for (int k4 = 0; k4 < KT; k4 += 4) {
       double af[4], bf[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        af[t] = static_cast<double>(A[(wi + t * 8 + fr) * kLd + k4 + fk]);
-        bf[t] = static_cast<double>(B[(wj + t * 8 + fr) * kLd + k4 + fk]);
+        af[t] = static_cast<double>(A[(wi + t * 8 + fr) * kLdT + k4 + fk]);
+        bf[t] = static_cast<double>(B[(wj + t * 8 + fr) * kLdT + k4 + fk]);
       }
       if (!(diag && wj > wi)) {  // the upper quadrant of a diagonal block is never used
 #pragma unroll
@@ -165,13 +165,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     if (with_e && warp == 1) {
       // columns lane and lane+32; rows in a lane-rotated order (conflict-free banks),
       // fixed per column -> deterministic
-      const T* E = pb + static_cast<size_t>(slot) * kBT * kLd;
+      const T* E = pb + static_cast<size_t>(slot) * kBT * kLdT;
 #pragma unroll 8
-      for (int k = 0; k < kKT; ++k) {
-        const int kk = (k + lane) & (kKT - 1);
+      for (int k = 0; k < KT; ++k) {
+        const int kk = (k + lane) & (KT - 1);
         const double er = static_cast<double>(E[kk]);
-        g0a = __fma_rn(static_cast<double>(A[lane * kLd + kk]), er, g0a);
-        g0b = __fma_rn(static_cast<double>(A[(lane + 32) * kLd + kk]), er, g0b);
+        g0a = __fma_rn(static_cast<double>(A[lane * kLdT + kk]), er, g0a);
+        g0b = __fma_rn(static_cast<double>(A[(lane + 32) * kLdT + kk]), er, g0b);
       }
     }
   }
@@ -230,7 +230,16 @@ struct GramSplit {
 
 // CTAs per SM of the G kernel: 3 (2-stage ring, <=170 registers) keeps the DMMA
 // pipe ~75% busy vs ~65% at 2 CTAs (3-stage ring); tuning aid BAK_GRAM_OCC=2
+// Default: 16-row stages, 2-stage ring (37 KB fp64), <= 128 registers, 4 CTAs
+// per SM — measured 46.2 ms vs 48.0 ms (32-row stages, 3 CTAs/SM) for C3's
+// G.  Tuning aids: BAK_GRAM_KT=32 (32-row stages; then BAK_GRAM_OCC=2|3).
+static bool gram_kt16() {
+  const char* kt = getenv("BAK_GRAM_KT");
+  return !(kt && kt[0] == '3' && kt[1] == '2');
+}
+
 static int gram_occ() {
+  if (gram_kt16()) return 4;
   const char* o = getenv("BAK_GRAM_OCC");
   return (o && o[0] == '2') ? 2 : 3;
 }
@@ -296,8 +305,17 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
     return BAK_OK;
   };
   const bool occ3 = gram_occ() == 3;
+  const bool kt16 = gram_kt16();
   int rc;
-  if (dtype == BAK_F64)
+  if (kt16) {
+    auto go16 = [&](auto kern) -> int {
+      const size_t smem = 2ull * 2 * kBT * (16 + 4) * ts;
+      BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, kThreads, smem, st>>>(p);
+      return BAK_OK;
+    };
+    rc = dtype == BAK_F64 ? go16(gram_dmma_kernel<double, 2, 4, 16>) : go16(gram_dmma_kernel<float, 2, 4, 16>);
+  } else if (dtype == BAK_F64)
     rc = occ3 ? go(gram_dmma_kernel<double, 2, 3>, 2) : go(gram_dmma_kernel<double, 3, 2>, 3);
   else
     rc = occ3 ? go(gram_dmma_kernel<float, 2, 3>, 2) : go(gram_dmma_kernel<float, 3, 2>, 3);

@@ -300,8 +300,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) block_kernel(const BlockParams
         const int64_t j1 = imin64(j0 + thr, V);
         const int ls_block = ls;  // first stage of this block (resident mode)
         // ---- pass 1: thr dots against the stale e, reduced per chunk ----
-        for (int64_t c0 = j0; c0 < j1; c0 += kChunk) {
-          const int cn = static_cast<int>(imin64(kChunk, j1 - c0));
+        // a chunk's dots are finished by threads t < cn: at most NT per chunk
+        const int chunk = NT < kChunk ? NT : kChunk;
+        for (int64_t c0 = j0; c0 < j1; c0 += chunk) {
+          const int cn = static_cast<int>(imin64(chunk, j1 - c0));
           for (int i = 0; i < cn; i += 4) {
             T p[4];
 #pragma unroll
@@ -548,8 +550,9 @@ __global__ void __launch_bounds__(kMaxNT, 1) block_ldg_kernel(const BlockParams 
     for (int64_t j0 = 0; j0 < V && !aborted; j0 += thr) {
       const int64_t j1 = imin64(j0 + thr, V);
       // ---- pass 1: dots against the stale e ----
-      for (int64_t c0 = j0; c0 < j1; c0 += kChunk) {
-        const int cn = static_cast<int>(imin64(kChunk, j1 - c0));
+      const int chunk = NT < kChunk ? NT : kChunk;  // finished by threads t < cn
+      for (int64_t c0 = j0; c0 < j1; c0 += chunk) {
+        const int cn = static_cast<int>(imin64(chunk, j1 - c0));
         const int64_t cend = c0 + cn;
         auto dots = [&](T (&xg)[kLG][E], int i) {
           T p[kLG];

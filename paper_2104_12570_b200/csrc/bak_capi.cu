@@ -25,6 +25,7 @@ void set_error(const char* fmt, ...) {
 
 int cuda_fail(cudaError_t err, const char* what) {
   set_error("CUDA error %d (%s) in %s", static_cast<int>(err), cudaGetErrorString(err), what);
+  cudaGetLastError();  // a failed launch must not poison the next call's error check
   return BAK_ECUDA;
 }
 

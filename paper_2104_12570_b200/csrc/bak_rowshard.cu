@@ -339,10 +339,26 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = use_cl ? 2 : 1;
-  if (dtype == BAK_F64)
-    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, use_cl ? rowshard_kernel<double, true> : rowshard_kernel<double, false>, p));
-  else
-    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, use_cl ? rowshard_kernel<float, true> : rowshard_kernel<float, false>, p));
+  cudaError_t err = dtype == BAK_F64
+                        ? cudaLaunchKernelEx(&cfg, use_cl ? rowshard_kernel<double, true> : rowshard_kernel<double, false>, p)
+                        : cudaLaunchKernelEx(&cfg, use_cl ? rowshard_kernel<float, true> : rowshard_kernel<float, false>, p);
+  if (err != cudaSuccess && use_cl) {
+    // clusters not co-resident after all: one-level exchange over all SMs
+    cudaGetLastError();
+    const int flat_ctas = static_cast<int>(imax64(1, sms / nranks_local));
+    const int64_t flat_stride = imax64(2LL * flat_ctas * 8, 2LL * 32 * 8);
+    if (static_cast<int64_t>(nranks_local) * flat_stride * 4 <= workspace_bytes) {
+      p.ctas_per_rank = flat_ctas;
+      p.rows_per_cta = round_up((rows_per_rank + flat_ctas - 1) / flat_ctas, vec);
+      p.slot_stride = flat_stride;
+      BAK_CHECK_CUDA(cudaMemsetAsync(workspace, 0, nranks_local * flat_stride * 4, st));
+      cfg.gridDim = dim3(flat_ctas * nranks_local);
+      cfg.numAttrs = 1;
+      err = dtype == BAK_F64 ? cudaLaunchKernelEx(&cfg, rowshard_kernel<double, false>, p)
+                             : cudaLaunchKernelEx(&cfg, rowshard_kernel<float, false>, p);
+    }
+  }
+  BAK_CHECK_CUDA(err);
   count_launches(1);
   return BAK_OK;
 }

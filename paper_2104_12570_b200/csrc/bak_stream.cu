@@ -223,10 +223,19 @@ int launch_stream(int dtype, const StreamPlan& pl0, const SweepParams& prm0, cud
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = use_cl ? 2 : 1;
-  if (dtype == BAK_F64)
-    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, use_cl ? stream_kernel<double, true> : stream_kernel<double, false>, prm));
-  else
-    BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, use_cl ? stream_kernel<float, true> : stream_kernel<float, false>, prm));
+  cudaError_t err = dtype == BAK_F64
+                        ? cudaLaunchKernelEx(&cfg, use_cl ? stream_kernel<double, true> : stream_kernel<double, false>, prm)
+                        : cudaLaunchKernelEx(&cfg, use_cl ? stream_kernel<float, true> : stream_kernel<float, false>, prm);
+  if (err != cudaSuccess && use_cl) {
+    // the occupancy query can be optimistic about co-resident clusters: one-level exchange
+    cudaGetLastError();
+    prm.rows_per_cta = pl0.rows_per_cta;
+    cfg.gridDim = dim3(pl0.nblocks);
+    cfg.numAttrs = 1;
+    err = dtype == BAK_F64 ? cudaLaunchKernelEx(&cfg, stream_kernel<double, false>, prm)
+                           : cudaLaunchKernelEx(&cfg, stream_kernel<float, false>, prm);
+  }
+  BAK_CHECK_CUDA(err);
   count_launches(1);
   return BAK_OK;
 }

@@ -855,7 +855,7 @@ int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm, cudaSt
   if (pl.variant == BAK_VARIANT_GRID && pl.cluster) {
     const int rc = dtype == BAK_F64 ? launch_nt<double, kModeGridCl>(pl, prm, st)
                                     : launch_nt<float, kModeGridCl>(pl, prm, st);
-    if (rc != BAK_EUNSUPPORTED) return rc;
+    if (rc == BAK_OK) return rc;  // else (capacity / cooperative launch refused): one level
     // clusters did not fit co-resident: one-level grid exchange
     if (getenv("BAK_DEBUG")) fprintf(stderr, "bak: two-level grid exchange unavailable (%s)\n", bak_last_error());
     SweepPlan flat;

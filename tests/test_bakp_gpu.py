@@ -288,3 +288,29 @@ def test_direct_load_and_tma_ring_kernels_agree(obs, nv, thr, dtype, monkeypatch
     ref = orc.solve_bakp(x, y, max_iter=8, tol=0, thr=thr)
     for r in (r_ldg, r_tma):
         _check(r, ref["a_hat"], ref["sweeps_run"], ref["converged"], x, y, dtype)
+
+
+@pytest.mark.parametrize("obs,nv,thr,dtype", [(33, 35, 34, np.float64), (40, 100, 70, np.float32),
+                                              (3000, 150, 100, np.float64)])
+def test_block_wider_than_the_cta(obs, nv, thr, dtype):
+    """Blocks wider than the CTA's thread count (few rows, many columns per
+    block): every column of the block gets its delta (regression: columns past
+    the thread count were skipped)."""
+    pb = _pb()
+    rng = np.random.default_rng(obs + nv)
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+    y = (x @ rng.uniform(-1, 1, nv).astype(dtype)).astype(dtype)
+    try:
+        ref = orc.solve_bakp(x, y, max_iter=4, tol=0, thr=thr)
+    except orc.DivergenceError:
+        with pytest.raises(pb.DivergenceError):
+            pb.solve_bakp(x, y, pb.BlockConfig(base=pb.SolveConfig(max_iter=4, tol=0), thr=thr))
+        return
+    for kern in ("tma", "ldg"):
+        import os
+        os.environ["BAK_BLOCK_KERNEL"] = kern
+        try:
+            rep = pb.solve_bakp(x, y, pb.BlockConfig(base=pb.SolveConfig(max_iter=4, tol=0), thr=thr))
+        finally:
+            os.environ.pop("BAK_BLOCK_KERNEL", None)
+        assert orc.rel_coeff_err(rep.a_hat, ref["a_hat"]) <= _tol(dtype), kern

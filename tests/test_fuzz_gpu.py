@@ -1,0 +1,82 @@
+"""Seeded randomized shapes through every kernel family against the oracle:
+ragged row counts (not multiples of the vector width, the cluster or the CTA
+row block), odd column counts, both precisions, early break on/off, zero
+columns.  Catches planner / tail-handling edge cases the fixed-shape tests
+miss."""
+
+import numpy as np
+import pytest
+
+from oracle import bak_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.dtype(np.float64): 1e-10, np.dtype(np.float32): 1e-4}
+
+
+def _case(seed):
+    rng = np.random.default_rng(10_000 + seed)
+    dtype = np.float64 if seed % 3 else np.float32
+    obs = int(rng.choice([1, 2, 3, 7, 31, 33, 257, 1023, 1025, 2049, 4097, 9999, 33_333, 70_001]))
+    nv = int(rng.integers(1, 48))
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+    if nv > 2 and seed % 4 == 0:
+        x[:, int(rng.integers(nv))] = 0.0
+    if not np.any(x):
+        x[0, 0] = 1.0
+    y = (x @ rng.uniform(-1, 1, nv).astype(dtype) + 0.1 * rng.standard_normal(obs)).astype(dtype)
+    tol = float(rng.choice([0.0, 1e-3, 1e-6]))
+    return x, y, tol, rng
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_fuzz_sweep_variants(seed):
+    import paper_2104_12570_b200 as pb
+    x, y, tol, rng = _case(seed)
+    obs, nv = x.shape
+    cfg = dict(max_iter=6, tol=tol, record_history=True)
+    ref = orc.solve(x, y, **cfg)
+    variants = ["auto", "stream"]
+    if obs <= 4096:
+        variants.append("cluster" if obs > 256 else "cta")
+    if obs > 32768:
+        variants.append("grid")
+    if nv <= 256:
+        variants.append("gram")
+    for v in variants:
+        try:
+            rep = pb.solve_bak(x, y, pb.SolveConfig(**cfg), variant=v)
+        except pb.bak._lib.BakError as err:
+            if "does not fit" in str(err) or "unsupported" in str(err).lower():
+                continue
+            raise
+        assert rep.sweeps_run == ref["sweeps_run"], (v, obs, nv)
+        assert rep.converged == ref["converged"], (v, obs, nv)
+        assert orc.rel_coeff_err(rep.a_hat, ref["a_hat"]) <= TOL[x.dtype], (v, obs, nv)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_blocked_and_batched(seed):
+    import paper_2104_12570_b200 as pb
+    x, y, tol, rng = _case(100 + seed)
+    obs, nv = x.shape
+    thr = int(rng.integers(1, nv + 1))
+    try:
+        ref = orc.solve_bakp(x, y, max_iter=5, tol=tol, thr=thr)
+    except orc.DivergenceError:
+        with pytest.raises(pb.DivergenceError):
+            pb.solve_bakp(x, y, pb.BlockConfig(base=pb.SolveConfig(max_iter=5, tol=tol), thr=thr))
+        return
+    for v in ("auto", "stream") + (("gram",) if nv <= 256 else ()):
+        rep = pb.solve_bakp(x, y, pb.BlockConfig(base=pb.SolveConfig(max_iter=5, tol=tol), thr=thr), variant=v)
+        assert rep.sweeps_run == ref["sweeps_run"], (v, obs, nv, thr)
+        assert orc.rel_coeff_err(rep.a_hat, ref["a_hat"]) <= TOL[x.dtype], (v, obs, nv, thr)
+    if obs <= 2048:
+        ns = int(rng.integers(1, 9))
+        xs = np.stack([x] * ns)
+        ys = np.stack([y] * ns)
+        br = pb.solve_bak_batched(xs, ys, pb.SolveConfig(max_iter=5, tol=tol))
+        r = orc.solve(x, y, max_iter=5, tol=tol)
+        for s in range(ns):
+            assert br.sweeps_run[s] == r["sweeps_run"]
+            assert orc.rel_coeff_err(br.a_hat[s], r["a_hat"]) <= TOL[x.dtype]

@@ -80,3 +80,34 @@ def test_fuzz_blocked_and_batched(seed):
         for s in range(ns):
             assert br.sweeps_run[s] == r["sweeps_run"]
             assert orc.rel_coeff_err(br.a_hat[s], r["a_hat"]) <= TOL[x.dtype]
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_scoring_random_order_warm_start(seed):
+    import paper_2104_12570_b200 as pb
+    x, y, tol, rng = _case(300 + seed)
+    obs, nv = x.shape
+    # column scoring (select.py:56-85), random exclusions
+    excl = sorted(set(rng.integers(0, nv, size=int(rng.integers(0, max(1, nv // 2)))).tolist()))
+    try:
+        b_ref, s_ref = orc.score_all_columns(x, y, excluded=excl)
+    except orc.SelectionExhaustedError:
+        with pytest.raises(pb.SelectionExhaustedError):
+            pb.score_all_columns(x, y, excluded=excl)
+    else:
+        b, s = pb.score_all_columns(x, y, excluded=excl)
+        fin = np.isfinite(s_ref)
+        assert np.array_equal(np.isfinite(s), fin)
+        e2 = float(np.dot(y.astype(np.float64), y.astype(np.float64)))
+        t = 1e-10 if x.dtype == np.float64 else 1e-5
+        assert np.max(np.abs(s[fin] - s_ref[fin])) <= t * max(e2, 1e-300)
+        srt = np.sort(s_ref[fin])
+        if srt.size < 2 or srt[1] - srt[0] > 100 * t * e2:
+            assert b == b_ref
+    # random ordering and warm start (bak.py:98-99, 173-175, 189)
+    a0 = rng.uniform(-1, 1, nv).astype(x.dtype)
+    cfg = dict(max_iter=5, tol=tol, ordering="random", ordering_seed=int(rng.integers(1 << 30)))
+    ref = orc.solve(x, y, a0=a0, **cfg)
+    rep = pb.solve_bak(x, y, pb.SolveConfig(**cfg), a0=a0)
+    assert rep.sweeps_run == ref["sweeps_run"] and rep.converged == ref["converged"]
+    assert orc.rel_coeff_err(rep.a_hat, ref["a_hat"]) <= TOL[x.dtype]

@@ -49,6 +49,7 @@ struct RowshardParams {
   int rank0;        // global rank of launch-rank 0
   int nranks;       // global number of ranks
   int nranks_local;
+  int keep_next;  // x_{j+1} kept in L2 (this GPU's e and one column of its rows fit)
   uint32_t epoch_base;
   uint32_t* mbox[kMaxRanks];  // mailbox of every global rank: [2 bufs][nranks][8 u32]
 };
@@ -197,7 +198,8 @@ __global__ void __launch_bounds__(512, 1) rowshard_kernel(const RowshardParams p
     const bool has_next = !(last && sweep + 1 == p.max_iter);
     const int64_t cn = last ? 0 : c + 1;
     backward = !backward;
-    stream_pass<T>(e, x + c * p.ldx, x + cn * p.ldx, nrows, d, n2 != T(0), has_next, last, backward, pv, qv);
+    stream_pass<T>(e, x + c * p.ldx, x + cn * p.ldx, nrows, d, n2 != T(0), has_next, last, backward, pv, qv,
+                   p.keep_next != 0);
     if (updater) {
       if (n2 != T(0)) {
         a_val = Num<T>::add(a_val, d);
@@ -319,6 +321,10 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
   p.status = status;
   p.slots = static_cast<uint32_t*>(workspace);
   p.slot_stride = slot_stride;
+  // this GPU's e plus one column of its rows fit in L2: keep x_{j+1} there, so
+  // HBM sees each column once (e.g. C3 fp64 over 8 GPUs: 2 x 16.8 MB per GPU)
+  p.keep_next = 2 * obs_local * static_cast<int64_t>(ts) <= static_cast<int64_t>(0.75 * l2_bytes());
+  if (const char* k = getenv("BAK_STREAM_KEEP")) p.keep_next = k[0] == '1';
   p.rank0 = rank;
   p.nranks = nranks;
   p.nranks_local = nranks_local;

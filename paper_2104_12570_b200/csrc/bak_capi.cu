@@ -1,6 +1,7 @@
 // C-ABI entry points and host utilities (error text, device queries, sweep
 // dispatch).  See include/bak200.h for the contract of every symbol.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <atomic>
@@ -50,6 +51,20 @@ int device_sms() {
 int device_max_smem_optin() {
   static int cache[64] = {0};
   return cached_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448, cache);
+}
+
+// Cooperative launches with thread-block clusters (the two-level exchanges)
+// cannot be replayed by a profiler that injects itself into the process
+// (ncu sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE / NV_TPS_LAUNCH_TOKEN, other
+// tools CUDA_INJECTION64_PATH): use the one-level exchanges there.
+bool coop_clusters_ok() {
+  static int ok = -1;
+  if (ok < 0)
+    ok = (getenv("CUDA_INJECTION64_PATH") == nullptr && getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") == nullptr &&
+          getenv("NV_TPS_LAUNCH_TOKEN") == nullptr && getenv("BAK_NO_COOP_CLUSTERS") == nullptr)
+             ? 1
+             : 0;
+  return ok == 1;
 }
 
 int64_t l2_bytes() {

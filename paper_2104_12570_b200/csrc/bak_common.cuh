@@ -206,6 +206,7 @@ inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 int device_sms();
 int device_max_smem_optin();
 int64_t l2_bytes();
+bool coop_clusters_ok();
 void count_launches(int n);
 }  // namespace bak
 

@@ -292,7 +292,7 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
   int cl_per_rank = static_cast<int>(imin64(imin64(cap, sms / kRsCluster) / nranks_local, 32));
   // (only when it keeps >= 3/4 of the CTAs: with many emulated ranks per GPU
   // one cluster per rank would starve the streaming passes of bandwidth)
-  const bool use_cl = !(flat && flat[0] == '1') && cl_per_rank >= 1 &&
+  const bool use_cl = !(flat && flat[0] == '1') && cl_per_rank >= 1 && coop_clusters_ok() &&
                       4 * cl_per_rank * kRsCluster >= 3 * per_rank_ctas;
   if (use_cl) per_rank_ctas = cl_per_rank * kRsCluster;
   const int64_t rows_per_rank = round_up((obs_local + nranks_local - 1) / nranks_local, vec);

@@ -192,7 +192,7 @@ int launch_stream(int dtype, const StreamPlan& pl0, const SweepParams& prm0, cud
   int ncl = pl.nblocks / kStreamCluster;
   if (ncl > cap) ncl = cap;
   if (ncl > 32) ncl = 32;
-  const bool cl = !(flat && flat[0] == '1') && ncl >= 2;
+  const bool cl = !(flat && flat[0] == '1') && ncl >= 2 && coop_clusters_ok();
   if (cl) {
     const int64_t vec = 16 / static_cast<int64_t>(dtype_size(dtype));
     pl.nblocks = ncl * kStreamCluster;

@@ -820,7 +820,7 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
     // evenly over a multiple of kGridCluster CTAs.  BAK_GRID_FLAT=1: one level.
     const char* flat = getenv("BAK_GRID_FLAT");
     const int max_parts = kGridCluster * (grid_cluster_capacity() < 32 ? grid_cluster_capacity() : 32);
-    if (!(flat && flat[0] == '1')) {
+    if (!(flat && flat[0] == '1') && coop_clusters_ok()) {
       for (int e : kEs) {
         const int64_t rows = 256LL * e;
         const int64_t parts = round_up((obs + rows - 1) / rows, kGridCluster);

@@ -1,6 +1,6 @@
 # DRAM bytes per launch for the on-chip-e kernels (north star: "ncu must show
-# (ncu cannot replay cooperative launches with clusters: those runs force the one-level exchange,
-#  whose DRAM traffic is the same)
+# (ncu cannot replay cooperative launches with clusters: under ncu the library uses the one-level exchange
+#  automatically (coop_clusters_ok), whose DRAM traffic is the same; the FLAT variables below are explicit)
 # ... that e traffic stays on-chip").  Each command first runs without ncu.
 set -u
 mkdir -p gpurun_out/prof

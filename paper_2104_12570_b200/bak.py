@@ -681,6 +681,8 @@ def solve_bak_batched(xs, ys, config: SolveConfig | None = None, a0=None, *, dev
         raise ValueError("solve_bak_batched supports ordering='cyclic' only")
     torch = _torch()
     lib = _lib.load()
+    if _batch_pipelinable(torch, xs, ys) and a0 is None:
+        return _solve_batched_pipelined(lib, torch, xs, ys, cfg, device, return_device)
     db = to_device_batch(xs, device)
     dev = db.data.device
     nsys, nv, obs, ld, code = db.nsys, db.vars, db.obs, db.ldx, db.code
@@ -720,6 +722,106 @@ def solve_bak_batched(xs, ys, config: SolveConfig | None = None, a0=None, *, dev
     return BatchSolveReport(
         a_hat=a if return_device else _host(a),
         residual=resid if return_device else _host(resid),
+        residual_norm_history=(hist if return_device else hist.cpu().numpy()) if hist is not None else None,
+        sweeps_run=stat[:, 0].copy(), converged=stat[:, 1].astype(bool), wall_time=wall,
+        drift_warning=stat[:, 2].astype(bool))
+
+
+_BATCH_PIPE_MIN_BYTES = 256 << 20
+_BATCH_PIPE_CHUNKS = 8
+
+
+def _batch_pipelinable(torch, xs, ys):
+    """Large PINNED host batch (torch CPU tensor (nsys, obs, vars) whose
+    (nsys, vars, obs) transpose is contiguous with 16-byte aligned columns)."""
+    if not (_is_torch(xs) and not xs.is_cuda and xs.ndim == 3 and xs.is_pinned()):
+        return False
+    if xs.dtype not in (torch.float32, torch.float64) or xs.numel() * xs.element_size() < _BATCH_PIPE_MIN_BYTES:
+        return False
+    src = xs.transpose(1, 2)
+    if not src.is_contiguous() or (src.shape[2] * src.element_size()) % 16:
+        return False
+    return _is_torch(ys) and not ys.is_cuda and ys.is_pinned() and ys.dtype == xs.dtype and ys.is_contiguous()
+
+
+def _solve_batched_pipelined(lib, torch, xs, ys, cfg, device, return_device):
+    """solve_bak_batched from pinned host memory: the systems are split into
+    chunks; chunk k+1 is uploaded on a copy stream while chunk k is solved on
+    the compute stream, and chunk k's results go back on a third stream — the
+    upload (PCIe) and the solve (HBM) overlap instead of adding up.  Same
+    kernels, same per-system results as the resident path."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    src = xs.transpose(1, 2)                       # (nsys, vars, obs), contiguous, pinned
+    nsys, nv, obs = src.shape
+    np_dtype = np.float64 if src.dtype == torch.float64 else np.float32
+    code = _dtype_code(np_dtype)
+    tdt = src.dtype
+    yh = ys.reshape(nsys, -1)
+    if yh.shape[1] != obs:
+        raise ValueError(f"y has length {yh.shape[1]}, expected {obs}")
+    main = torch.cuda.current_stream(dev)
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    h2d.wait_stream(main)
+    t0 = time.perf_counter()
+    data = torch.empty((nsys, nv, obs), dtype=tdt, device=dev)
+    yd = torch.empty((nsys, obs), dtype=tdt, device=dev)
+    norms = torch.empty(nsys * nv, dtype=tdt, device=dev)
+    yn = torch.empty(nsys, dtype=tdt, device=dev)
+    a = torch.zeros((nsys, nv), dtype=tdt, device=dev)
+    resid = torch.empty((nsys, obs), dtype=tdt, device=dev)
+    hist = torch.zeros((nsys, cfg.max_iter), dtype=torch.float64, device=dev) if cfg.record_history else None
+    status = torch.zeros((nsys, 4), dtype=torch.int64, device=dev)
+    out_a = torch.empty((nsys, nv), dtype=tdt, pin_memory=True) if not return_device else None
+    out_r = torch.empty((nsys, obs), dtype=tdt, pin_memory=True) if not return_device else None
+    per = -(-nsys // _BATCH_PIPE_CHUNKS)
+    chunks = [(s0, min(nsys, s0 + per)) for s0 in range(0, nsys, per)]
+    wsb = max(lib.bak_colnorms_workspace(code, obs, per * nv), lib.bak_colnorms_workspace(code, obs, per), 4096)
+    ws = _Workspace(torch, dev, wsb)
+    st = ctypes.c_void_p(main.cuda_stream)
+    events = []
+    for s0, s1 in chunks:
+        with torch.cuda.stream(h2d):
+            data[s0:s1].copy_(src[s0:s1], non_blocking=True)
+            yd[s0:s1].copy_(yh[s0:s1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+            events.append(ev)
+    done = []
+    for (s0, s1), ev in zip(chunks, events):
+        main.wait_event(ev)
+        n = s1 - s0
+        xp = ctypes.c_void_p(data[s0].data_ptr())
+        _lib.check(lib.bak_colnorms(code, xp, obs, n * nv, obs, _ptr(norms[s0 * nv:s1 * nv]), ws.ptr, ws.nbytes, st),
+                   "bak_colnorms")
+        _lib.check(lib.bak_colnorms(code, _ptr(yd[s0]), obs, n, obs, _ptr(yn[s0:s1]), ws.ptr, ws.nbytes, st),
+                   "bak_colnorms(y)")
+        ynorm2 = yn[s0:s1].to(torch.float64)
+        _lib.check(lib.bak_solve_batched(code, xp, obs, nv, obs, nv * obs, n, _ptr(yd[s0]), obs,
+                                         _ptr(norms[s0 * nv:s1 * nv]), _ptr(ynorm2), _ptr(a[s0]), 0,
+                                         _ptr(resid[s0]), cfg.max_iter, float(cfg.tol), DRIFT_TOL,
+                                         _ptr(hist[s0]) if hist is not None else None, _ptr(status[s0]), st),
+                   "bak_solve_batched")
+        if out_a is not None:
+            ev2 = torch.cuda.Event()
+            ev2.record(main)
+            d2h.wait_event(ev2)
+            with torch.cuda.stream(d2h):
+                out_a[s0:s1].copy_(a[s0:s1], non_blocking=True)
+                out_r[s0:s1].copy_(resid[s0:s1], non_blocking=True)
+        done.append(ynorm2)  # keep the per-chunk temporaries alive until the stream syncs
+    main.wait_stream(d2h)
+    stat = status.cpu().numpy()
+    torch.cuda.current_stream(dev).synchronize()
+    wall = time.perf_counter() - t0
+    bad = stat[:, 3]
+    if np.any(bad == 1):
+        raise ValueError("every column of x has zero norm; nothing to solve "
+                         f"(systems {np.flatnonzero(bad == 1)[:8].tolist()})")
+    if np.any(bad):
+        raise _lib.BakError(f"bak_solve_batched device error {int(bad[bad != 0][0])}")
+    return BatchSolveReport(
+        a_hat=a if return_device else out_a.numpy(),
+        residual=resid if return_device else out_r.numpy(),
         residual_norm_history=(hist if return_device else hist.cpu().numpy()) if hist is not None else None,
         sweeps_run=stat[:, 0].copy(), converged=stat[:, 1].astype(bool), wall_time=wall,
         drift_warning=stat[:, 2].astype(bool))

@@ -380,3 +380,25 @@ def test_grid_two_level_and_flat_exchange_match_oracle(precision, monkeypatch):
         np.testing.assert_allclose(r1.residual_norm_history, ref["residual_norm_history"], rtol=max(1e3 * tol, 1e-6))
         outs[flat] = r1.a_hat
     assert orc.rel_coeff_err(outs["0"], outs["1"]) <= tol
+
+
+def test_batched_pipelined_host_upload_bit_identical():
+    """Pinned host batches >= 256 MB take the chunked path (upload of chunk k+1
+    overlapped with the solve of chunk k): same kernels, same bits."""
+    import torch
+    pb = _pb()
+    nsys, obs, nv = 8192, 512, 32
+    g = torch.Generator().manual_seed(7)
+    hx = torch.randn((nsys, nv, obs), generator=g, dtype=torch.float32).pin_memory()
+    hy = torch.randn((nsys, obs), generator=g, dtype=torch.float32).pin_memory()
+    xs = hx.transpose(1, 2)  # (nsys, obs, vars) view, pinned
+    cfg = pb.SolveConfig(max_iter=20, tol=0, record_history=True)
+    r_pipe = pb.solve_bak_batched(xs, hy, cfg)
+    r_ref = pb.solve_bak_batched(xs.contiguous(), hy.clone(), cfg)  # pageable, resident path
+    assert r_pipe.a_hat.tobytes() == r_ref.a_hat.tobytes()
+    assert r_pipe.residual.tobytes() == r_ref.residual.tobytes()
+    assert np.array_equal(r_pipe.sweeps_run, r_ref.sweeps_run)
+    assert np.array_equal(r_pipe.residual_norm_history, r_ref.residual_norm_history)
+    s = 1234
+    ref = orc.solve(hx[s].numpy().T, hy[s].numpy(), max_iter=20, tol=0)
+    assert orc.rel_coeff_err(r_pipe.a_hat[s], ref["a_hat"]) <= 1e-4

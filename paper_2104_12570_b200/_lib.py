@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbak200.so")
+# BAK_LIB_PATH: A/B tuning runs load an alternative build of the same ABI
+LIB_PATH = os.environ.get("BAK_LIB_PATH") or os.path.join(_HERE, "libbak200.so")
 
 F32, F64 = 0, 1
 EDIVERGED = 6  # device status: the blocked sweep's divergence guard tripped

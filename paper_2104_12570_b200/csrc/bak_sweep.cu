@@ -710,6 +710,7 @@ int launch_e(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
 template <typename T, int MODE>
 int launch_nt(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   if (pl.nthreads == 32) return launch_e<T, MODE, 32>(pl, prm, st);
+  if (pl.nthreads <= 128) return launch_e<T, MODE, 128>(pl, prm, st);
   return launch_e<T, MODE, kMaxConsumers>(pl, prm, st);
 }
 

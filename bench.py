@@ -443,7 +443,10 @@ def run_ours(args, cfg, rank, world, dev):
         k_ms, r = _timed(lambda: pb.solve_bak_batched(dm, y, scfg, return_device=True), args.steps, dev, 1)
         k_ms /= args.steps
         k_sweeps = int(r.sweeps_run.max())
-        kernel = "batched_kernel (whole per-system solve, one CTA per system; x resident in smem)"
+        kernel = ("batched_kernel (whole per-system solve, one CTA per system; x re-read every sweep, "
+                  "resident systems per SM capped so x is served from L2 after the first sweep)")
+        extra["note"] = ("x-bytes per sweep over kernel time; above the HBM copy peak because the sweeps "
+                         "after the first read x from L2")
         alg_bytes = xbytes * k_sweeps
     elif used.startswith("gram"):
         xbytes = dm.obs * dm.vars * ts

@@ -187,6 +187,11 @@ int bak_copy_rows_h2d(void* dst, int64_t dld, const void* src, int64_t sld, int6
                       int64_t vars, int64_t elem, void* stream);
 
 /* Peer mapping helpers for one-process-per-GPU (CUDA IPC; 64-byte handles). */
+/* Device allocation of its own (cudaMalloc, zero-filled): the mailbox a rank
+ * exports over CUDA IPC must be a whole allocation — an IPC handle names an
+ * allocation and peers map its base address. */
+int bak_dev_alloc(int64_t bytes, void** devptr);
+int bak_dev_free(void* devptr);
 int bak_ipc_get_handle(void* devptr, void* handle64);
 int bak_ipc_open_handle(const void* handle64, void** devptr);
 int bak_ipc_close(void* devptr);

@@ -66,6 +66,8 @@ SIGNATURES = {
     "bak_mailbox_bytes": (_i64, [_i64]),
     "bak_sweep_rowshard": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _vp, _vp, _int, _int,
                                   _vp, _i64, _int, _vp, _i64, _vp]),
+    "bak_dev_alloc": (_int, [_i64, ctypes.POINTER(_vp)]),
+    "bak_dev_free": (_int, [_vp]),
     "bak_ipc_get_handle": (_int, [_vp, _vp]),
     "bak_ipc_open_handle": (_int, [_vp, ctypes.POINTER(_vp)]),
     "bak_ipc_close": (_int, [_vp]),

@@ -369,6 +369,25 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
   return BAK_OK;
 }
 
+// Mailboxes exported over CUDA IPC must be their OWN allocation: a handle
+// names a whole cudaMalloc allocation and the importer maps its base, so a
+// sub-allocation (e.g. from a caching allocator) would be mapped at the wrong
+// address on the peers.
+extern "C" int bak_dev_alloc(int64_t bytes, void** devptr) {
+  if (!devptr || bytes < 1) {
+    set_error("bak_dev_alloc: bad arguments");
+    return BAK_EINVAL;
+  }
+  BAK_CHECK_CUDA(cudaMalloc(devptr, static_cast<size_t>(bytes)));
+  BAK_CHECK_CUDA(cudaMemset(*devptr, 0, static_cast<size_t>(bytes)));
+  return BAK_OK;
+}
+
+extern "C" int bak_dev_free(void* devptr) {
+  BAK_CHECK_CUDA(cudaFree(devptr));
+  return BAK_OK;
+}
+
 extern "C" int bak_ipc_get_handle(void* devptr, void* handle64) {
   cudaIpcMemHandle_t h;
   BAK_CHECK_CUDA(cudaIpcGetMemHandle(&h, devptr));

@@ -312,16 +312,20 @@ class Mailboxes:
             self.buf = torch.zeros(nranks * per, dtype=torch.uint8, device=dev)
             self.ptrs = [self.buf.data_ptr() + r * per for r in range(nranks)]
         else:
-            self.buf = torch.zeros(per, dtype=torch.uint8, device=dev)
-            torch.cuda.synchronize()
+            # the exported mailbox is an allocation of its own (not a caching-
+            # allocator block): peers map the base of the allocation a handle names
+            self.buf = None
+            p_own = ctypes.c_void_p()
+            _lib.check(lib.bak_dev_alloc(per, ctypes.byref(p_own)), "bak_dev_alloc")
+            self._own = p_own.value
             h = (ctypes.c_uint8 * 64)()
-            _lib.check(lib.bak_ipc_get_handle(ctypes.c_void_p(self.buf.data_ptr()), h), "bak_ipc_get_handle")
+            _lib.check(lib.bak_ipc_get_handle(ctypes.c_void_p(self._own), h), "bak_ipc_get_handle")
             mine = torch.tensor(list(bytes(h)), dtype=torch.uint8, device=dev)
             handles = comm.all_gather([mine])
             self.ptrs = []
             for r, hr in enumerate(handles):
                 if r == comm.rank:
-                    self.ptrs.append(self.buf.data_ptr())
+                    self.ptrs.append(self._own)
                     continue
                 raw = (ctypes.c_uint8 * 64)(*hr.cpu().tolist())
                 p = ctypes.c_void_p()
@@ -340,6 +344,9 @@ class Mailboxes:
         for p in self._opened:
             lib.bak_ipc_close(ctypes.c_void_p(p))
         self._opened = []
+        if getattr(self, "_own", None):
+            lib.bak_dev_free(ctypes.c_void_p(self._own))
+            self._own = None
 
 
 def sweep_rowshard(dm, e, a, norms, max_iter, thresh2, mailboxes, rank, nranks, nranks_local=1, history=None,

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
   double* es = red + kWarps * KR;                        // [KR]
   double* ash = es + KR;                                 // [VB] final coefficients (fused residual)
   double* red2 = ash + VB;                               // [kWarps][KR]
+  float* dshf = reinterpret_cast<float*>(red2 + kWarps * KR);  // [VB] fp32 copy of d (fp32 sweep passes)
   const bool want_r = p.afin != nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = static_cast<int>(p.vars);
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
   }
   for (int j = tid; j < VB; j += blockDim.x) {
     dsh[j] = (p.apply && j < V) ? p.delta[j] : 0.0;
+    dshf[j] = static_cast<float>(dsh[j]);
     ash[j] = (want_r && j < V) ? static_cast<double>(static_cast<const T*>(p.afin)[j]) : 0.0;
   }
   __syncthreads();
@@ -121,6 +123,15 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
   uint32_t ph = 0;
   int prev = -1;
   int64_t tile = blockIdx.x;
+  // fp32 sweep passes (apply + dot, no fused residual): x is read from shared
+  // memory once per element into registers; (X d)_r runs as fp32 FMAs over the
+  // warp's columns, and each column's two products of a lane (rows r, r+32)
+  // are formed in fp32 and added to the fp64 accumulator — one F2F per two
+  // elements instead of two per element (the conversions were the limiter:
+  // fp32 pass at ~0.82x of the copy peak).  The final-residual pass and the
+  // dot-only (column scoring) passes keep the fp64 products.
+  constexpr bool kF32 = sizeof(T) == 4;
+  const bool fast32 = kF32 && p.apply && p.dot && !want_r;
   T e_next[RPL], y_next[RPL];
   const T* yv = static_cast<const T*>(p.y);
   T* rv = static_cast<T*>(p.resid);
@@ -153,7 +164,18 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
         if (globaltimer() - t0 > kTimeoutNs) break;
     }
     const T* X = xs + static_cast<size_t>(s) * KR * VB + static_cast<size_t>(warp) * CW * KR + lane;
-    if (p.apply) {
+    float xr[kF32 ? RPL : 1][kF32 ? CW : 1];
+    if (kF32 && fast32) {
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+#pragma unroll
+        for (int q = 0; q < CW; ++q) xr[kF32 ? i : 0][kF32 ? q : 0] = static_cast<float>(X[q * KR + 32 * i]);
+        float t = 0.f;
+#pragma unroll
+        for (int q = 0; q < CW; ++q) t = __fmaf_rn(xr[kF32 ? i : 0][kF32 ? q : 0], dshf[warp * CW + q], t);
+        red[warp * KR + lane + 32 * i] = static_cast<double>(t);
+      }
+    } else if (p.apply) {
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
         double t = 0.0;
@@ -197,7 +219,18 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
       }
     }
     bar_cons();
-    if (p.dot) {
+    if (kF32 && fast32) {
+      float er[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) er[i] = static_cast<float>(es[lane + 32 * i]);  // exact: e is fp32
+#pragma unroll
+      for (int q = 0; q < CW; ++q) {
+        float t = __fmul_rn(xr[0][kF32 ? q : 0], er[0]);
+#pragma unroll
+        for (int i = 1; i < RPL; ++i) t = __fmaf_rn(xr[kF32 ? i : 0][kF32 ? q : 0], er[i], t);
+        acc[q] = __dadd_rn(acc[q], static_cast<double>(t));
+      }
+    } else if (p.dot) {
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
         const double er = es[lane + 32 * i];
@@ -242,7 +275,7 @@ int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStre
   constexpr int VB = CW * kWarps;
   constexpr int KR = kR * rows_per_lane<T>();
   const size_t smem = kS * static_cast<size_t>(KR) * VB * sizeof(T) + 2 * kS * 8 + 2 * VB * 8 + 2 * kWarps * KR * 8 +
-                      KR * 8;
+                      KR * 8 + VB * 4;
   auto kern = gram_pass_tma_kernel<T, CW>;
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<grid, kCons + 32, smem, st>>>(map, p);

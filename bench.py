@@ -576,7 +576,12 @@ def run_ours(args, cfg, rank, world, dev):
                 else:
                     r = pb.solve_bak(hxv, hy, scfg, variant=variant)
                 return r, r.a_hat.nbytes + r.residual.nbytes + dm.vars * ts + 64
-        e2e_step()
+        # warm-up: two calls whose results are alive together, as in the timed
+        # loop (the previous step's result is held while the next one runs) —
+        # the caching host allocator then holds the pinned result buffers and
+        # no timed step pays a first-time cudaHostAlloc
+        keep = [e2e_step(), e2e_step()]
+        del keep
         ems, (r, d2h) = _timed(e2e_step, args.steps, dev, world)
         e2e = {"value": round(sweeps_per_step * args.steps / (ems / 1e3), 3), "unit": "sweeps/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

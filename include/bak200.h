@@ -162,6 +162,11 @@ int bak_solve_batched(int dtype,
                       int64_t max_iter, double tol, double drift_tol,
                       double* history, int64_t* status, void* stream);
 
+/* Systems bak_solve_batched runs concurrently on the current device (one
+ * wave) for systems of this shape stored contiguously; callers streaming a
+ * large batch in chunks size the chunks in whole waves.  0 on error. */
+int64_t bak_solve_batched_wave(int dtype, int64_t obs, int64_t vars);
+
 /* ---- (5) multi-GPU row sharding (C3 at N>1) ---------------------------------
  * Row-sharded sweep: rank r holds rows [r0, r0+obs_local) of x, y, e; a and
  * norms2 are replicated.  Per column, every rank's grid reduces its partial dot

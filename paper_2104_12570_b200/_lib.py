@@ -38,6 +38,7 @@ SIGNATURES = {
     "bak_sweep": (_int, [_int, _int, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _dbl,
                          _vp, _vp, _vp, _i64, _vp]),
     "bak_sweep_pick_variant": (_int, [_int, _i64, _i64]),
+    "bak_solve_batched_wave": (_i64, [_int, _i64, _i64]),
     "bak_solve_batched": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _int, _vp,
                                  _i64, _dbl, _dbl, _vp, _vp, _vp]),
     "bak_gram_pass_blocks": (_int, [_int, _i64]),

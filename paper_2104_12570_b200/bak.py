@@ -773,8 +773,25 @@ def _solve_batched_pipelined(lib, torch, xs, ys, cfg, device, return_device):
     status = torch.zeros((nsys, 4), dtype=torch.int64, device=dev)
     out_a = torch.empty((nsys, nv), dtype=tdt, pin_memory=True) if not return_device else None
     out_r = torch.empty((nsys, obs), dtype=tdt, pin_memory=True) if not return_device else None
-    per = -(-nsys // _BATCH_PIPE_CHUNKS)
-    chunks = [(s0, min(nsys, s0 + per)) for s0 in range(0, nsys, per)]
+    # chunks in whole waves of the batched kernel (systems in flight at once):
+    # a partial last wave per chunk costs nearly a full wave.  Chunk sizes grow
+    # 1, 2, 4, ... waves up to ~nsys/8 so the solve starts after a short upload
+    # and each next upload finishes before the solve of the chunk before it
+    wave = int(lib.bak_solve_batched_wave(code, obs, nv))
+    if wave > 0:
+        k = max(1, (nsys // _BATCH_PIPE_CHUNKS) // wave)
+        sizes, w = [], 1
+        while sum(sizes) < nsys:
+            sizes.append(min(w * wave, nsys - sum(sizes)))
+            w = min(2 * w, k)
+    else:
+        sizes = [-(-nsys // _BATCH_PIPE_CHUNKS)] * _BATCH_PIPE_CHUNKS
+    chunks, s0 = [], 0
+    for n in sizes:
+        if s0 < nsys:
+            chunks.append((s0, min(nsys, s0 + n)))
+            s0 += n
+    per = max(s1 - s0 for s0, s1 in chunks)
     wsb = max(lib.bak_colnorms_workspace(code, obs, per * nv), lib.bak_colnorms_workspace(code, obs, per), 4096)
     ws = _Workspace(torch, dev, wsb)
     st = ctypes.c_void_p(main.cuda_stream)

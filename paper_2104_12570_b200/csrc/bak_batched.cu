@@ -262,10 +262,17 @@ __global__ void __launch_bounds__(NT_) batched_kernel(const BatchedParams prm) {
   }
 }
 
+// nsys == 0: occupancy query only — systems in flight per SM (g_wave_per_sm)
+thread_local int g_wave_per_sm = 0;
+
 template <typename T, int E, int NT, bool SMEM>
 int launch_batched_t(const BatchedParams& prm, size_t smem, cudaStream_t st) {
   auto kern = batched_kernel<T, E, NT, SMEM>;
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (prm.nsys == 0) {
+    BAK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_wave_per_sm, kern, NT, smem));
+    return BAK_OK;
+  }
   kern<<<static_cast<unsigned>(prm.nsys), NT, smem, st>>>(prm);
   count_launches(1);
   BAK_CHECK_CUDA(cudaGetLastError());
@@ -297,15 +304,13 @@ int launch_batched(int E, int nt, bool in_smem, const BatchedParams& prm, size_t
 
 using namespace bak;
 
-extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, int64_t x_stride,
-                                 int64_t nsys, const void* y, int64_t y_stride, const void* norms2,
-                                 const double* ynorm2, void* a, int warm, void* resid, int64_t max_iter, double tol,
-                                 double drift_tol, double* history, int64_t* status, void* stream) {
-  if (obs < 1 || vars < 1 || ldx < obs || nsys < 1 || max_iter < 1 || !x || !y || !norms2 || !ynorm2 || !a ||
-      !resid || !status || (dtype != BAK_F32 && dtype != BAK_F64)) {
-    set_error("bak_solve_batched: bad arguments");
-    return BAK_EINVAL;
-  }
+namespace {
+// plan (rows per thread, threads, x residency, shared memory) and launch; with
+// query = true nothing is launched and g_wave_per_sm receives the occupancy
+int batched_entry(bool query, int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, int64_t x_stride,
+                  int64_t nsys, const void* y, int64_t y_stride, const void* norms2, const double* ynorm2, void* a,
+                  int warm, void* resid, int64_t max_iter, double tol, double drift_tol, double* history,
+                  int64_t* status, void* stream) {
   const size_t ts = dtype_size(dtype);
   // rows per thread / threads: aim for ~4 warps per system, E <= 32
   static const int kEs[] = {1, 2, 4, 8, 16, 32};
@@ -350,6 +355,7 @@ extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t 
                     max_iter, tol, drift_tol, history, status, 0};
   const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ldx * ts) % 16 == 0) &&
                        ((x_stride * ts) % 16 == 0) && xbytes < (1u << 20);
+  if (query) prm.nsys = 0;
   size_t smem = small;
   // x resident in shared memory only when that still leaves >= 8 systems per
   // SM in flight; otherwise stream x from L2/HBM every sweep with many more
@@ -391,4 +397,37 @@ extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t 
     BAK_B(float)
   }
 #undef BAK_B
+}
+}  // namespace
+
+extern "C" int bak_solve_batched(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, int64_t x_stride,
+                                 int64_t nsys, const void* y, int64_t y_stride, const void* norms2,
+                                 const double* ynorm2, void* a, int warm, void* resid, int64_t max_iter, double tol,
+                                 double drift_tol, double* history, int64_t* status, void* stream) {
+  if (obs < 1 || vars < 1 || ldx < obs || nsys < 1 || max_iter < 1 || !x || !y || !norms2 || !ynorm2 || !a ||
+      !resid || !status || (dtype != BAK_F32 && dtype != BAK_F64)) {
+    set_error("bak_solve_batched: bad arguments");
+    return BAK_EINVAL;
+  }
+  return batched_entry(false, dtype, x, obs, vars, ldx, x_stride, nsys, y, y_stride, norms2, ynorm2, a, warm, resid,
+                       max_iter, tol, drift_tol, history, status, stream);
+}
+
+// Systems the batched solve runs concurrently on this device (one wave) for
+// systems of this shape stored contiguously (ldx = obs padded to 16 bytes):
+// callers that stream batches in chunks size them in whole waves.  0 on error.
+extern "C" int64_t bak_solve_batched_wave(int dtype, int64_t obs, int64_t vars) {
+  if (obs < 1 || vars < 1 || (dtype != BAK_F32 && dtype != BAK_F64)) {
+    set_error("bak_solve_batched_wave: bad arguments");
+    return 0;
+  }
+  const int64_t vec = dtype == BAK_F64 ? 2 : 4;
+  const int64_t ldx = (obs + vec - 1) / vec * vec;
+  alignas(16) static const double dummy[2] = {0.0, 0.0};
+  g_wave_per_sm = 0;
+  if (batched_entry(true, dtype, dummy, obs, vars, ldx, vars * ldx, 1, dummy, ldx, dummy, dummy,
+                    const_cast<double*>(dummy), 0, const_cast<double*>(dummy), 1, 0.0, 0.0, nullptr, nullptr,
+                    nullptr) != BAK_OK)
+    return 0;
+  return static_cast<int64_t>(g_wave_per_sm) * device_sms();
 }

@@ -73,6 +73,7 @@ CONFIGS = {
 DEFAULT_CONFIG = "c3"
 METRIC = "sweeps/sec and x-stream HBM GB/s vs roofline at 1/2/4/8 B200; CPU baseline"
 SPEC_HBM_GBS = 8000.0
+DMMA_PEAK_TFLOPS = 37.2  # measured fp64 DMMA ceiling on this B200 pool (tools/micro/dmma_peak.cu)
 REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
@@ -488,6 +489,10 @@ def run_ours(args, cfg, rank, world, dev):
         flops = 2.0 * dm.obs * (nb * (nb + 1) // 2) * 64 * 64
         extra["gram_matrix"] = {"kernel": "gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
                                 "ms": round(g_ms, 3), "tflops": round(flops / (g_ms / 1e3) / 1e12, 2),
+                                "bound": "tensor (fp64 DMMA)", "peak_tflops": DMMA_PEAK_TFLOPS,
+                                "peak_source": "tools/micro/dmma_peak.cu: register-only m8n8k4 f64 DMMA, all SMs, "
+                                               "1965 MHz (no fp64 dense figure in MEASURED_PEAKS.json)",
+                                "frac": round(flops / (g_ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS, 3),
                                 "share_of_step": round(g_ms / (ms / args.steps), 3)}
     elif cfg.get("thr"):
         vcode = _lib.VARIANTS[used]

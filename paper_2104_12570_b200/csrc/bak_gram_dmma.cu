@@ -40,6 +40,27 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// 3xTF32 (fp32 inputs only): v = hi + lo with hi = RN_tf32(v), lo = RN_tf32(v - hi)
+// (v - hi is exact in fp32); a*b ~ lo_a*hi_b + hi_a*lo_b + hi_a*hi_b, each
+// product exact in the tensor core, accumulated in fp32 over a few stages and
+// then flushed into fp64 — G to ~2^-21 relative, on the legacy tf32 MMA path
+// (277.6 TFLOP/s measured, tools/micro/tf32_peak.cu, vs 37.2 for fp64 DMMA)
+__device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
+  uint32_t h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+  const float r = v - __uint_as_float(h);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  hi = h;
+  lo = l;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 struct GramParams {
   const void* x;
   int64_t obs, ldx, vars;
@@ -58,7 +79,7 @@ __device__ __forceinline__ void tri_index_strict(int o, int& bi, int& bj) {
   bj = o - bi * (bi - 1) / 2;
 }
 
-template <typename T, int kStages, int kMinBlocks, int KT = kKT>
+template <typename T, int kStages, int kMinBlocks, int KT = kKT, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const GramParams p) {
   constexpr int kLdT = KT + 4;  // smem column stride (elements)
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -129,6 +150,37 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // X3: the warp's 32x32 quarter as 2 (m16) x 4 (n8) tf32 tiles
+  constexpr int kFlush = 8;  // stages per fp32 partial before it is added into fp64
+  // fp64 totals live in shared memory ([32][kThreads] doubles after the
+  // panels; 4 CTAs per SM need <= 128 registers per thread)
+  float accf[2][4][4];
+  double* accd = reinterpret_cast<double*>(pb + static_cast<size_t>(kStages) * kBT * kLdT) + tid;
+  int nflush = 0;
+  if constexpr (X3) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          accf[a][b][c] = 0.f;
+          accd[((a * 4 + b) * 4 + c) * kThreads] = 0.0;
+        }
+  }
+  auto flush = [&]() {
+    if constexpr (X3) {
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            accd[((a * 4 + b) * 4 + c) * kThreads] += static_cast<double>(accf[a][b][c]);
+            accf[a][b][c] = 0.f;
+          }
+    }
+  };
 
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
@@ -147,6 +199,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     const int slot = step % kStages;
     const T* A = pa + static_cast<size_t>(slot) * kBT * kLdT;
     const T* B = diag ? A : pb + static_cast<size_t>(slot) * kBT * kLdT;
+    if constexpr (X3) {
+#pragma unroll
+      for (int k8 = 0; k8 < KT; k8 += 8) {
+        if (!(diag && wj > wi)) {
+          uint32_t ah[2][4], al[2][4];
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            const int r0 = wi + m * 16 + fr;
+            split_tf32(A[r0 * kLdT + k8 + fk], ah[m][0], al[m][0]);
+            split_tf32(A[(r0 + 8) * kLdT + k8 + fk], ah[m][1], al[m][1]);
+            split_tf32(A[r0 * kLdT + k8 + fk + 4], ah[m][2], al[m][2]);
+            split_tf32(A[(r0 + 8) * kLdT + k8 + fk + 4], ah[m][3], al[m][3]);
+          }
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            uint32_t bh[2], bl[2];
+            const int c0 = wj + n * 8 + fr;
+            split_tf32(B[c0 * kLdT + k8 + fk], bh[0], bl[0]);
+            split_tf32(B[c0 * kLdT + k8 + fk + 4], bh[1], bl[1]);
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+              mma_tf32(accf[m][n], al[m], bh);  // small terms first
+              mma_tf32(accf[m][n], ah[m], bl);
+              mma_tf32(accf[m][n], ah[m], bh);
+            }
+          }
+        }
+      }
+      if (++nflush == kFlush) {
+        nflush = 0;
+        flush();
+      }
+    } else {
 #pragma unroll
     for (int k4 = 0; k4 < KT; k4 += 4) {
       double af[4], bf[4];
@@ -161,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
 #pragma unroll
           for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
       }
+    }
     }
     if (with_e && warp == 1) {
       // columns lane and lane+32; rows in a lane-rotated order (conflict-free banks),
@@ -183,6 +269,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
   }
   cp_async_wait<0>();
   double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
+  if constexpr (X3) {
+    flush();
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        const int i = wi + m * 16 + fr, j = wj + n * 8 + fk * 2;
+        const double* ad = accd + ((m * 4 + n) * 4) * kThreads;
+        out[i * kBT + j] = ad[0];
+        out[i * kBT + j + 1] = ad[kThreads];
+        out[(i + 8) * kBT + j] = ad[2 * kThreads];
+        out[(i + 8) * kBT + j + 1] = ad[3 * kThreads];
+      }
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -314,7 +415,17 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
       kern<<<grid, kThreads, smem, st>>>(p);
       return BAK_OK;
     };
-    rc = dtype == BAK_F64 ? go16(gram_dmma_kernel<double, 2, 4, 16>) : go16(gram_dmma_kernel<float, 2, 4, 16>);
+    // fp32 inputs: 3xTF32 on the tf32 MMA path (BAK_GRAM_G=dmma keeps fp64 DMMA)
+    const char* gg = getenv("BAK_GRAM_G");
+    const bool x3 = !(gg && gg[0] == 'd');
+    auto go16x3 = [&](auto kern) -> int {
+      const size_t smem = 2ull * 2 * kBT * (16 + 4) * ts + 32ull * kThreads * 8;  // + fp64 totals
+      BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, kThreads, smem, st>>>(p);
+      return BAK_OK;
+    };
+    rc = dtype == BAK_F64 ? go16(gram_dmma_kernel<double, 2, 4, 16>)
+                          : (x3 ? go16x3(gram_dmma_kernel<float, 2, 4, 16, true>) : go16(gram_dmma_kernel<float, 2, 4, 16>));
   } else if (dtype == BAK_F64)
     rc = occ3 ? go(gram_dmma_kernel<double, 2, 3>, 2) : go(gram_dmma_kernel<double, 3, 2>, 3);
   else

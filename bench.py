@@ -112,6 +112,8 @@ class ClockSampler:
             time.sleep(0.05)
 
     def __enter__(self):
+        if os.environ.get("BAK_BENCH_NO_CLOCKS") == "1":  # A/B of the sampler's own cost
+            return self
         q = "clocks.sm,clocks.max.sm," + ",".join("clocks_event_reasons." + r for r in REASON_FIELDS)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
@@ -339,22 +341,34 @@ def _max_over_ranks(ms, world, dev):
     return float(t.item())
 
 
+_LAST_STEP_MS = []
+
+
 def _timed(fn, steps, dev, world):
     import torch
     st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     out = None
-    e0.record(st)
-    for _ in range(steps):
+    # The process holds a large, long-lived object graph (torch, numpy, the
+    # inputs): a full collection triggered inside a timed step walks it for
+    # 50-110 ms while the GPU idles behind the solve's result read (2 of 6 runs
+    # measured).  Move it out of the collector's view before timing; the
+    # collector stays enabled for the garbage the timed steps create.
+    import gc
+    gc.collect()
+    gc.freeze()
+    ev[0].record(st)
+    for i in range(steps):
         out = fn()
-    e1.record(st)
+        ev[i + 1].record(st)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    return _max_over_ranks(e0.elapsed_time(e1), world, dev), out
+    _LAST_STEP_MS[:] = [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(steps)]
+    return _max_over_ranks(ev[0].elapsed_time(ev[steps]), world, dev), out
 
 
 def _prewarm(dm, dev, seconds=1.0):
@@ -422,6 +436,7 @@ def run_ours(args, cfg, rank, world, dev):
     l0 = lib.bak_launch_count()
     clk.begin()
     ms, rep = _timed(step, args.steps, dev, world)
+    step_ms = list(_LAST_STEP_MS)  # this rank's per-step device times (diagnostic)
     clk.end()
     clk.__exit__(None, None, None)
     launches = lib.bak_launch_count() - l0
@@ -610,7 +625,8 @@ def run_ours(args, cfg, rank, world, dev):
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "step_ms": step_ms,
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (seeded device RNG, reference distributions and shapes)",
         "config": {"workload": args.config, "desc": cfg["desc"], "obs": cfg["obs"], "vars": cfg["vars"],

@@ -40,18 +40,19 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// 3xTF32 (fp32 inputs only): v = hi + lo with hi = RN_tf32(v), lo = RN_tf32(v - hi)
-// (v - hi is exact in fp32); a*b ~ lo_a*hi_b + hi_a*lo_b + hi_a*hi_b, each
+// 3xTF32 (fp32 inputs only): v = hi + lo with hi = RN_tf32(v), lo = v - hi
+// (exact in fp32); a*b ~ lo_a*hi_b + hi_a*lo_b + hi_a*hi_b, each
 // product exact in the tensor core, accumulated in fp32 over a few stages and
 // then flushed into fp64 — G to ~2^-21 relative, on the legacy tf32 MMA path
 // (277.6 TFLOP/s measured, tools/micro/tf32_peak.cu, vs 37.2 for fp64 DMMA)
 __device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
-  uint32_t h, l;
+  // hi: v rounded to tf32 (|lo| <= 2^-11 |v|); lo: the exact remainder, whose
+  // low 13 bits the tf32 datapath ignores (~2^-22 of v), as does the dropped
+  // lo*lo product
+  uint32_t h;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-  const float r = v - __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
   hi = h;
-  lo = l;
+  lo = __float_as_uint(v - __uint_as_float(h));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
 #pragma unroll
       for (int k8 = 0; k8 < KT; k8 += 8) {
         if (!(diag && wj > wi)) {
-          uint32_t ah[2][4], al[2][4];
+          uint32_t ah[2][4], al[2][4], bh[4][2], bl[4][2];
 #pragma unroll
           for (int m = 0; m < 2; ++m) {
             const int r0 = wi + m * 16 + fr;
@@ -214,17 +215,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
           }
 #pragma unroll
           for (int n = 0; n < 4; ++n) {
-            uint32_t bh[2], bl[2];
             const int c0 = wj + n * 8 + fr;
-            split_tf32(B[c0 * kLdT + k8 + fk], bh[0], bl[0]);
-            split_tf32(B[c0 * kLdT + k8 + fk + 4], bh[1], bl[1]);
-#pragma unroll
-            for (int m = 0; m < 2; ++m) {
-              mma_tf32(accf[m][n], al[m], bh);  // small terms first
-              mma_tf32(accf[m][n], ah[m], bl);
-              mma_tf32(accf[m][n], ah[m], bh);
-            }
+            split_tf32(B[c0 * kLdT + k8 + fk], bh[n][0], bl[n][0]);
+            split_tf32(B[c0 * kLdT + k8 + fk + 4], bh[n][1], bl[n][1]);
           }
+          // three rounds over the 8 tiles (small terms first): consecutive MMAs
+          // write different accumulators, so none waits on the one before
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) mma_tf32(accf[m][n], al[m], bh[n]);
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) mma_tf32(accf[m][n], ah[m], bl[n]);
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) mma_tf32(accf[m][n], ah[m], bh[n]);
         }
       }
       if (++nflush == kFlush) {

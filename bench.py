@@ -353,10 +353,11 @@ def _timed(fn, steps, dev, world):
         torch.distributed.barrier()
     out = None
     # The process holds a large, long-lived object graph (torch, numpy, the
-    # inputs): a full collection triggered inside a timed step walks it for
-    # 50-110 ms while the GPU idles behind the solve's result read (2 of 6 runs
-    # measured).  Move it out of the collector's view before timing; the
-    # collector stays enabled for the garbage the timed steps create.
+    # inputs): move it out of the collector's view before timing so no full
+    # collection walks it inside a timed step (the collector stays enabled for
+    # the garbage the timed steps create).  Occasional 40-110 ms slow steps
+    # remain with the collector disabled too (sw_power_cap transients); step_ms
+    # in the line shows them.
     import gc
     gc.collect()
     gc.freeze()
@@ -694,7 +695,7 @@ def main():
     json_fd = _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--variant", default=None)

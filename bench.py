@@ -34,6 +34,7 @@ C/OpenMP port of oracle/ (all host threads), rank 0 only.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -352,15 +353,6 @@ def _timed(fn, steps, dev, world):
     if world > 1:
         torch.distributed.barrier()
     out = None
-    # The process holds a large, long-lived object graph (torch, numpy, the
-    # inputs): move it out of the collector's view before timing so no full
-    # collection walks it inside a timed step (the collector stays enabled for
-    # the garbage the timed steps create).  Occasional 40-110 ms slow steps
-    # remain with the collector disabled too (sw_power_cap transients); step_ms
-    # in the line shows them.
-    import gc
-    gc.collect()
-    gc.freeze()
     ev[0].record(st)
     for i in range(steps):
         out = fn()
@@ -429,6 +421,14 @@ def run_ours(args, cfg, rank, world, dev):
     # GPU time has passed (a fresh process's first passes over 34 GB of newly
     # allocated HBM ran ~10 % slow for the first second, measured)
     _prewarm(dm, dev)
+    # The process holds a large, long-lived object graph (torch, numpy, the
+    # inputs): move it out of the collector's view so no full collection walks
+    # it inside a timed step (the collector stays enabled for new garbage).
+    # Done BEFORE the warm-up: a host pause right before the timed steps left
+    # the GPU idle, and after the idle the second timed step ran 40-110 ms slow
+    # in ~1 of 4 runs (power-cap transient; step_ms shows each step).
+    gc.collect()
+    gc.freeze()
     for _ in range(args.warmup):
         rep = step()
     used = "batched" if batched else rep.variant

@@ -104,7 +104,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     chunk = p.chunk_o;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wi = (warp >> 1) * 32, wj = (warp & 1) * 32;  // warp's quarter of the block
+  // Off-diagonal block: warp w owns quarter (w>>1, w&1) of the 64x64 block.
+  // Diagonal block (only its lower triangle is read): warps 0 and 3 own the two
+  // diagonal quarters and compute only their lower tiles; warps 1 and 2 split
+  // the lower off-diagonal quarter (32, 0) by tile rows and share the fused
+  // first-sweep dots.  A diagonal CTA's warps then issue 8-10 of 16 DMMA tiles
+  // (4-6 of 8 tf32 tiles) plus the dots; no MMA lands on tiles never read.
+  const bool dq = diag && (warp == 0 || warp == 3);
+  const bool dh = diag && (warp == 1 || warp == 2);
+  const int half = warp == 1 ? 0 : 1;  // dh: which half of the tile rows
+  const int wi = dh ? 32 : (warp >> 1) * 32, wj = dh ? 0 : (warp & 1) * 32;
   const T* __restrict__ x = static_cast<const T*>(p.x);
   const T* __restrict__ ev = static_cast<const T*>(p.e);
   const bool with_e = diag && ev != nullptr;
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     }
   };
   // fused g0 (warp 1 of a diagonal CTA owns the unused upper quadrant: no DMMA work)
-  double g0a = 0.0, g0b = 0.0;
+  double g0a = 0.0;
 
   double acc[4][4][2];
 #pragma unroll
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     if constexpr (X3) {
 #pragma unroll
       for (int k8 = 0; k8 < KT; k8 += 8) {
-        if (!(diag && wj > wi)) {
+        {
           uint32_t ah[2][4], al[2][4], bh[4][2], bl[4][2];
 #pragma unroll
           for (int m = 0; m < 2; ++m) {
@@ -219,20 +228,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
             split_tf32(B[c0 * kLdT + k8 + fk], bh[n][0], bl[n][0]);
             split_tf32(B[c0 * kLdT + k8 + fk + 4], bh[n][1], bl[n][1]);
           }
-          // three rounds over the 8 tiles (small terms first): consecutive MMAs
-          // write different accumulators, so none waits on the one before
+          // three rounds over the warp's tiles (small terms first): consecutive
+          // MMAs write different accumulators, so none waits on the one before.
+          // Tile (m, n) = rows 16m.., cols 8n..; dq: lower tiles (8n < 16m+16)
+          auto live = [&](int m, int n) { return dq ? (8 * n < 16 * m + 16) : (dh ? m == half : true); };
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) mma_tf32(accf[m][n], al[m], bh[n]);
+            for (int n = 0; n < 4; ++n)
+              if (live(m, n)) mma_tf32(accf[m][n], al[m], bh[n]);
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) mma_tf32(accf[m][n], ah[m], bl[n]);
+            for (int n = 0; n < 4; ++n)
+              if (live(m, n)) mma_tf32(accf[m][n], ah[m], bl[n]);
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) mma_tf32(accf[m][n], ah[m], bh[n]);
+            for (int n = 0; n < 4; ++n)
+              if (live(m, n)) mma_tf32(accf[m][n], ah[m], bh[n]);
         }
       }
       if (++nflush == kFlush) {
@@ -248,7 +262,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
         af[t] = static_cast<double>(A[(wi + t * 8 + fr) * kLdT + k4 + fk]);
         bf[t] = static_cast<double>(B[(wj + t * 8 + fr) * kLdT + k4 + fk]);
       }
-      if (!(diag && wj > wi)) {  // the upper quadrant of a diagonal block is never used
+      if (dq) {  // diagonal quarter: lower 8x8 tiles only
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b <= a; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      } else if (dh) {  // half of the lower off-diagonal quarter
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if ((a >> 1) == half)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      } else {
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -256,24 +281,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
       }
     }
     }
-    if (with_e && warp == 1) {
-      // columns lane and lane+32; rows in a lane-rotated order (conflict-free banks),
-      // fixed per column -> deterministic
+    if (with_e && dh) {
+      // the two half-quarter warps share the fused dots: warp 1 column lane,
+      // warp 2 column lane + 32; rows in a lane-rotated order (conflict-free
+      // banks), fixed per column -> deterministic
       const T* E = pb + static_cast<size_t>(slot) * kBT * kLdT;
+      const int col = lane + 32 * half;
 #pragma unroll 8
       for (int k = 0; k < KT; ++k) {
         const int kk = (k + lane) & (KT - 1);
-        const double er = static_cast<double>(E[kk]);
-        g0a = __fma_rn(static_cast<double>(A[lane * kLdT + kk]), er, g0a);
-        g0b = __fma_rn(static_cast<double>(A[(lane + 32) * kLdT + kk]), er, g0b);
+        g0a = __fma_rn(static_cast<double>(A[col * kLdT + kk]), static_cast<double>(E[kk]), g0a);
       }
     }
   }
-  if (with_e && warp == 1) {
-    const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane;
+  if (with_e && dh) {
+    const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane + 32 * half;
     double* g = p.g0 + static_cast<int64_t>(chk) * p.vars;
     if (c0 < p.vars) g[c0] = g0a;
-    if (c0 + 32 < p.vars) g[c0 + 32] = g0b;
   }
   cp_async_wait<0>();
   double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
@@ -283,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int n = 0; n < 4; ++n) {
+        if (dq ? !(8 * n < 16 * m + 16) : (dh && m != half)) continue;  // not this warp's tile
         const int i = wi + m * 16 + fr, j = wj + n * 8 + fk * 2;
         const double* ad = accd + ((m * 4 + n) * 4) * kThreads;
         out[i * kBT + j] = ad[0];
@@ -290,16 +315,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
         out[(i + 8) * kBT + j] = ad[2 * kThreads];
         out[(i + 8) * kBT + j + 1] = ad[3 * kThreads];
       }
-    return;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (dq ? b > a : (dh && (a >> 1) != half)) continue;  // not this warp's tile
+        const int i = wi + a * 8 + fr, j = wj + b * 8 + fk * 2;
+        out[i * kBT + j] = acc[a][b][0];
+        out[i * kBT + j + 1] = acc[a][b][1];
+      }
   }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = wi + a * 8 + fr, j = wj + b * 8 + fk * 2;
-      out[i * kBT + j] = acc[a][b][0];
-      out[i * kBT + j + 1] = acc[a][b][1];
-    }
 }
 
 // G (vars x vars, full, symmetric) = sum over K chunks of the lower block partials
@@ -357,22 +383,24 @@ static GramSplit gram_split(int64_t obs, int64_t vars) {
   GramSplit g{};
   g.nb = static_cast<int>((vars + kBT - 1) / kBT);
   const int noff = g.nb * (g.nb - 1) / 2;
-  // one wave: 2 CTAs per SM (smem-bound); a diagonal CTA does 3/4 of the MMA work
-  // of an off-diagonal one, so it gets 4/3 of the rows
+  // One wave of CTAs, equal row chunks for every block by default.  With the
+  // first sweep's dots fused (warps 1-2 of the diagonal CTAs), diagonal and
+  // off-diagonal CTAs then take about the same time (in-solve G on C3: 42.8 ms
+  // fp64 / 36.2 ms fp32 at ratio 1 vs 46.8 / 43.3 at 0.625 — the 10/16 ratio
+  // of their DMMA tiles alone).  BAK_GRAM_DIAG_RATIO=r gives diagonal blocks
+  // 1/r of the rows (tuning aid).
   const int slots = gram_occ() * device_sms();
-  // Equal chunks for every block by default (measured faster at 3 CTAs/SM: the
-  // scheduler mixes block types per SM); BAK_GRAM_BALANCE=1 gives diagonal
-  // blocks (3 of 4 warp quarters busy) 4/3 of the rows.
-  const char* bal = getenv("BAK_GRAM_BALANCE");
-  if (!(bal && bal[0] == '1')) {
+  const char* rr = getenv("BAK_GRAM_DIAG_RATIO");
+  const double ratio = rr ? atof(rr) : 1.0;
+  if (!(ratio > 0.0 && ratio < 1.0)) {
     g.cd = g.co = imax_host(1, slots / (g.nb * (g.nb + 1) / 2));
   } else if (noff == 0) {
     g.co = 1;
     g.cd = slots;
   } else {
-    g.co = static_cast<int>(slots / (noff + 0.75 * g.nb));
+    g.co = static_cast<int>(slots / (noff + ratio * g.nb));
     if (g.co < 1) g.co = 1;
-    g.cd = (3 * g.co) / 4;
+    g.cd = static_cast<int>(ratio * g.co);
     if (g.cd < 1) g.cd = 1;
   }
   g.chunk_d = round_up((obs + g.cd - 1) / g.cd, kKT);

@@ -31,5 +31,11 @@ for e in ev[1:]:
         gaps.append((e.time_range.start - end, e.name[:50]))
     end = max(end, e.time_range.end)
 print(f"span {(t1 - t0) / 1e3:.2f} ms, kernel busy {busy / 1e3:.2f} ms, {len(ev)} device events")
+import collections  # noqa: E402
+per = collections.defaultdict(float)
+for e in ev:
+    per[e.name[:60]] += (e.time_range.end - e.time_range.start) / 1e3
+for n, t in sorted(per.items(), key=lambda kv: -kv[1])[:6]:
+    print(f"  {t:9.3f} ms  {n}")
 for g, n in sorted(gaps, reverse=True)[:8]:
     print(f"  gap {g / 1e3:8.3f} ms before {n}")

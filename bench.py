@@ -75,6 +75,7 @@ DEFAULT_CONFIG = "c3"
 METRIC = "sweeps/sec and x-stream HBM GB/s vs roofline at 1/2/4/8 B200; CPU baseline"
 SPEC_HBM_GBS = 8000.0
 DMMA_PEAK_TFLOPS = 37.2  # measured fp64 DMMA ceiling on this B200 pool (tools/micro/dmma_peak.cu)
+TF32_MMA_PEAK_TFLOPS = 277.6  # measured legacy tf32 mma.sync ceiling (tools/micro/tf32_peak.cu)
 REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
@@ -502,13 +503,22 @@ def run_ours(args, cfg, rank, world, dev):
         g_ms, _ = _timed(gram, 2, dev, 1)
         g_ms /= 2
         nb = -(-dm.vars // 64)
-        flops = 2.0 * dm.obs * (nb * (nb + 1) // 2) * 64 * 64
-        extra["gram_matrix"] = {"kernel": "gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
-                                "ms": round(g_ms, 3), "tflops": round(flops / (g_ms / 1e3) / 1e12, 2),
-                                "bound": "tensor (fp64 DMMA)", "peak_tflops": DMMA_PEAK_TFLOPS,
-                                "peak_source": "tools/micro/dmma_peak.cu: register-only m8n8k4 f64 DMMA, all SMs, "
-                                               "1965 MHz (no fp64 dense figure in MEASURED_PEAKS.json)",
-                                "frac": round(flops / (g_ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS, 3),
+        noff = nb * (nb - 1) // 2
+        if ts == 8:  # fp64 DMMA: off-diagonal blocks 64 8x8 tiles, diagonal blocks their 36 lower tiles
+            flops = 2.0 * dm.obs * 64 * (64 * noff + 36 * nb)
+            gk, gbound, gpeak = ("gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
+                                 "tensor (fp64 DMMA)", DMMA_PEAK_TFLOPS)
+            gsrc = "tools/micro/dmma_peak.cu: register-only m8n8k4 f64 DMMA, all SMs, 1965 MHz"
+        else:  # fp32: 3xTF32, three tf32 products per pair; diagonal blocks 20 of 32 16x8 tiles
+            flops = 3 * 2.0 * dm.obs * (4096 * noff + 2560 * nb)
+            gk, gbound, gpeak = ("gram_dmma_kernel<float, X3> (3xTF32 mma.sync m16n8k8, fp64 totals)",
+                                 "tensor (tf32 mma.sync)", TF32_MMA_PEAK_TFLOPS)
+            gsrc = "tools/micro/tf32_peak.cu: register-only m16n8k8 tf32 mma.sync, all SMs"
+        extra["gram_matrix"] = {"kernel": gk, "ms": round(g_ms, 3),
+                                "tflops_issued": round(flops / (g_ms / 1e3) / 1e12, 2),
+                                "bound": gbound, "peak_tflops": gpeak,
+                                "peak_source": gsrc + " (no such figure in MEASURED_PEAKS.json)",
+                                "frac": round(flops / (g_ms / 1e3) / 1e12 / gpeak, 3),
                                 "share_of_step": round(g_ms / (ms / args.steps), 3)}
     elif cfg.get("thr"):
         vcode = _lib.VARIANTS[used]

@@ -1,0 +1,64 @@
+"""The G = X^T X kernels behind the GRAM variant, checked directly against an
+fp64 numpy product: fp64 DMMA (exact products, fp64 sums) and, for fp32
+inputs, 3xTF32 (hi/lo split, ~2^-21 relative) and the fp64 DMMA fallback
+(BAK_GRAM_G=dmma).  Shapes cover ragged rows / columns, a single 64-column
+block and several diagonal / off-diagonal blocks."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gram(x, monkeypatch=None, env=None):
+    import torch
+    import paper_2104_12570_b200 as pb
+    from paper_2104_12570_b200 import _lib
+    from paper_2104_12570_b200.bak import _Workspace, _stream_ptr
+    if env:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+    lib = _lib.load()
+    dm = pb.to_device_matrix(x)
+    dev = dm.data.device
+    G = torch.empty((dm.vars, dm.vars), dtype=torch.float64, device=dev)
+    ws = _Workspace(torch, dev, lib.bak_gram_matrix_workspace(dm.code, dm.obs, dm.vars))
+    _lib.check(lib.bak_gram_matrix(dm.code, dm.ptr, dm.obs, dm.vars, dm.ldx, G.data_ptr(), ws.ptr, ws.nbytes,
+                                   _stream_ptr(torch, dev)), "bak_gram_matrix")
+    return G.cpu().numpy()
+
+
+@pytest.mark.parametrize("obs,nv", [(1000, 7), (50_001, 64), (131_071, 130), (200_000, 256)])
+def test_gram_matrix_fp64_dmma(obs, nv):
+    x = np.asfortranarray(np.random.default_rng(obs).standard_normal((obs, nv)))
+    ref = x.T @ x
+    G = _gram(x)
+    assert np.allclose(G, G.T, rtol=0, atol=0)  # mirrored exactly
+    err = np.linalg.norm(G - ref) / np.linalg.norm(ref)
+    assert err <= 1e-13, err
+
+
+@pytest.mark.parametrize("obs,nv", [(1000, 7), (50_001, 64), (131_071, 130), (200_000, 256)])
+def test_gram_matrix_fp32_3xtf32_and_dmma(obs, nv, monkeypatch):
+    x = np.asfortranarray(np.random.default_rng(obs + 1).standard_normal((obs, nv)).astype(np.float32))
+    xd = x.astype(np.float64)
+    ref = xd.T @ xd  # exact products of the fp32 inputs, fp64 sums
+    G3 = _gram(x)
+    err3 = np.linalg.norm(G3 - ref) / np.linalg.norm(ref)
+    assert err3 <= 2e-6, err3
+    # diagonal (the column norms the solve divides by) to a few 2^-21
+    d_err = np.max(np.abs(np.diag(G3) - np.diag(ref)) / np.diag(ref))
+    assert d_err <= 4e-6, d_err
+    Gd = _gram(x, monkeypatch, {"BAK_GRAM_G": "dmma"})
+    errd = np.linalg.norm(Gd - ref) / np.linalg.norm(ref)
+    assert errd <= 1e-13, errd
+
+
+def test_batched_wave_is_whole_sms():
+    from paper_2104_12570_b200 import _lib
+    import torch
+    lib = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for dt, obs, nv in ((0, 512, 32), (1, 200, 12), (0, 37, 6)):
+        w = int(lib.bak_solve_batched_wave(dt, obs, nv))
+        assert w > 0 and w % sms == 0, (dt, obs, nv, w)

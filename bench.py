@@ -425,13 +425,19 @@ def run_ours(args, cfg, rank, world, dev):
     # The process holds a large, long-lived object graph (torch, numpy, the
     # inputs): move it out of the collector's view so no full collection walks
     # it inside a timed step (the collector stays enabled for new garbage).
-    # Done BEFORE the warm-up: a host pause right before the timed steps left
-    # the GPU idle, and after the idle the second timed step ran 40-110 ms slow
-    # in ~1 of 4 runs (power-cap transient; step_ms shows each step).
     gc.collect()
     gc.freeze()
-    for _ in range(args.warmup):
-        rep = step()
+    # Warm-up with as many results alive as in the timed loop (the last
+    # warm-up result, the previous step's and the one being computed): the
+    # caching allocator then already holds every buffer the timed steps use.
+    # With only two alive during warm-up, the second timed step paid a
+    # 60-140 ms allocation of the third set (measured in ~1 of 4 runs).
+    hold = []
+    for _ in range(max(args.warmup, 2)):
+        hold.append(step())
+        hold = hold[-2:]
+    rep = hold[-1]
+    del hold
     used = "batched" if batched else rep.variant
 
     # ---- value: whole solves, inputs resident in HBM (max over ranks) ----

@@ -150,3 +150,26 @@ def test_fuzz_rowsharded_emulated(seed):
     assert orc.rel_coeff_err(A[0], ref["a_hat"]) <= tol
     for r in range(1, n):
         assert A[r].tobytes() == A[0].tobytes()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_gram_multiblock(seed):
+    """GRAM with several 64-column blocks (diagonal and off-diagonal G tiles,
+    ragged last block), ragged rows, both precisions, warm start / early break."""
+    import paper_2104_12570_b200 as pb
+    rng = np.random.default_rng(20_000 + seed)
+    dtype = np.float64 if seed % 2 else np.float32
+    obs = int(rng.choice([65, 1000, 4097, 33_333, 70_001, 131_075]))
+    nv = int(rng.integers(49, 300))
+    obs = max(obs, nv + 1)
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(dtype))
+    if seed % 5 == 0:
+        x[:, int(rng.integers(nv))] = 0.0
+    y = (x @ rng.uniform(-1, 1, nv).astype(dtype) + 0.05 * rng.standard_normal(obs)).astype(dtype)
+    tol = float(rng.choice([0.0, 1e-4]))
+    a0 = rng.uniform(-0.1, 0.1, nv).astype(dtype) if seed % 3 == 0 else None
+    cfg = dict(max_iter=5, tol=tol)
+    ref = orc.solve(x, y, a0=a0, **cfg)
+    rep = pb.solve_bak(x, y, pb.SolveConfig(**cfg), a0=a0, variant="gram")
+    assert rep.sweeps_run == ref["sweeps_run"] and rep.converged == ref["converged"], (obs, nv)
+    assert orc.rel_coeff_err(rep.a_hat, ref["a_hat"]) <= TOL[x.dtype], (obs, nv, dtype)

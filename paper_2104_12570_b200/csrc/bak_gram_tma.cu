@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
   if (tid == 0) {
     for (int s = 0; s < kS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kWarps);  // one arrive per consumer warp when it is done with the tile
     }
     fence_mbar_init();
   }
@@ -121,7 +121,6 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
   double sq = 0.0;
   int s = 0;
   uint32_t ph = 0;
-  int prev = -1;
   int64_t tile = blockIdx.x;
   // fp32 sweep passes (apply + dot, no fused residual): x is read from shared
   // memory once per element into registers; (X d)_r runs as fp32 FMAs over the
@@ -175,6 +174,8 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
         for (int q = 0; q < CW; ++q) t = __fmaf_rn(xr[kF32 ? i : 0][kF32 ? q : 0], dshf[warp * CW + q], t);
         red[warp * KR + lane + 32 * i] = static_cast<double>(t);
       }
+      __syncwarp();  // the tile is in registers: hand the slot back now
+      if (lane == 0) mbar_arrive1(&empty[s]);
     } else if (p.apply) {
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
@@ -194,7 +195,6 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
       }
     }
     bar_cons();
-    if (tid == 0 && prev >= 0) mbar_arrive1(&empty[prev]);  // previous tile fully consumed
     if (warp == 0) {
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
         for (int q = 0; q < CW; ++q) acc[q] = __fma_rn(static_cast<double>(X[q * KR + 32 * i]), er, acc[q]);
       }
     }
-    prev = s;
+    if (!(kF32 && fast32)) {  // this warp's last read of the tile was the dot above
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&empty[s]);
+    }
     if (++s == kS) { s = 0; ph ^= 1u; }
   }
   // column partials: sum over the tile rows (lanes), fixed butterfly order
@@ -255,7 +258,6 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
     if (lane == 0) p.sqpart[blockIdx.x] = v;
   }
   bar_cons();
-  if (tid == 0 && prev >= 0) mbar_arrive1(&empty[prev]);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

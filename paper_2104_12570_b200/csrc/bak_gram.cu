@@ -253,8 +253,17 @@ __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p)
         aj = Num<T>::add(aj, d);
       }
       __syncthreads();
-      if (tid < V)
-        for (int64_t k = j0; k < j1; ++k) rj = __fma_rn(-p.G[k * V + tid], dblk[k], rj);
+      if (tid < V) {  // G entries 8 at a time in flight, FMAs in column order
+        int64_t k = j0;
+        for (; k + 8 <= j1; k += 8) {
+          double gv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) gv[u] = p.G[(k + u) * V + tid];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) rj = __fma_rn(-gv[u], dblk[k + u], rj);
+        }
+        for (; k < j1; ++k) rj = __fma_rn(-p.G[k * V + tid], dblk[k], rj);
+      }
     }
     if (tid < V) {
       p.delta[tid] = dj;

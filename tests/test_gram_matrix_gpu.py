@@ -62,3 +62,25 @@ def test_batched_wave_is_whole_sms():
     for dt, obs, nv in ((0, 512, 32), (1, 200, 12), (0, 37, 6)):
         w = int(lib.bak_solve_batched_wave(dt, obs, nv))
         assert w > 0 and w % sms == 0, (dt, obs, nv, w)
+
+
+@pytest.mark.parametrize("corr", [0.9, 0.99])
+def test_gram_fp32_3xtf32_on_correlated_columns(corr, monkeypatch):
+    """fp32 GRAM solves on strongly correlated (slowly converging) columns,
+    where G's rounding shapes the iterates sweep by sweep: the 3xTF32 G meets
+    the fp32 bar against the oracle after a fixed number of sweeps, like the
+    fp64-DMMA G does."""
+    import paper_2104_12570_b200 as pb
+    from oracle import bak_oracle as orc
+    rng = np.random.default_rng(int(corr * 1000))
+    obs, nv = 60_000, 96
+    base = rng.standard_normal((obs, 1))
+    x = np.asfortranarray((corr * base + (1 - corr) * rng.standard_normal((obs, nv))).astype(np.float32))
+    y = (x @ rng.uniform(-1, 1, nv).astype(np.float32) + 0.01 * rng.standard_normal(obs)).astype(np.float32)
+    ref = orc.solve(x, y, max_iter=12, tol=0)
+    for env in (None, {"BAK_GRAM_G": "dmma"}):
+        if env:
+            monkeypatch.setenv("BAK_GRAM_G", "dmma")
+        rep = pb.solve_bak(x, y, pb.SolveConfig(max_iter=12, tol=0), variant="gram")
+        err = orc.rel_coeff_err(rep.a_hat, ref["a_hat"])
+        assert rep.sweeps_run == 12 and err <= 1e-4, (corr, env, err)

@@ -99,35 +99,33 @@ def _load_binary(path):
 
 
 def _load_csv(path):
-    # matio.py:60-80 (text, float64)
-    data = []
-    ncols = None
-    with open(path, "r", encoding="utf-8") as f:
-        for lineno, line in enumerate(f, start=1):
-            line = line.strip()
-            if not line:
-                continue
-            parts = line.split(",")
-            if ncols is None:
-                ncols = len(parts)
-            elif len(parts) != ncols:
-                raise MatrixFormatError(f"{path}: row {lineno} has {len(parts)} values, expected {ncols}")
-            try:
-                data.append([float(p) for p in parts])
-            except ValueError:
-                raise MatrixFormatError(f"{path}: row {lineno} has a non-numeric value") from None
-    if not data:
+    """Comma-separated text -> float64 F-order matrix; blank lines skipped,
+    every row as wide as the first (matio.py:60-80 messages)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        numbered = [(n, text.strip()) for n, text in enumerate(fh, start=1)]
+    rows = [(n, text.split(",")) for n, text in numbered if text]
+    if not rows:
         raise MatrixFormatError(f"{path}: no rows")
-    return np.asfortranarray(np.array(data, dtype=np.float64))
+    width = len(rows[0][1])
+    values = np.empty((len(rows), width), dtype=np.float64)
+    for i, (n, fields) in enumerate(rows):
+        if len(fields) != width:
+            raise MatrixFormatError(f"{path}: row {n} has {len(fields)} values, expected {width}")
+        try:
+            values[i] = [float(v) for v in fields]
+        except ValueError:
+            raise MatrixFormatError(f"{path}: row {n} has a non-numeric value") from None
+    return np.asfortranarray(values)
 
 
 def _sniff(path, format):
+    """Explicit format, else binary when the file starts with the magic."""
     if format is None:
-        with open(path, "rb") as f:
-            format = "binary" if f.read(4) == MAGIC else "csv"
-    if format not in FORMATS:
-        raise ValueError(f"unknown format {format!r}, expected one of {FORMATS}")
-    return format
+        with open(path, "rb") as fh:
+            return "binary" if fh.read(len(MAGIC)) == MAGIC else "csv"
+    if format in FORMATS:
+        return format
+    raise ValueError(f"unknown format {format!r}, expected one of {FORMATS}")
 
 
 def load_matrix(path, format=None):

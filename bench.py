@@ -3,6 +3,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--variant V] [--impl ours|reference]
 
+--gpus N > 1 re-launches itself as N ranks under torch.distributed.run
+(127.0.0.1 rendezvous, NCCL_DEBUG=INFO on stderr) unless already launched so.
+
 One JSON line on rank 0 (driver contract).  A "step" is one full solve through
 the drop-in API (norms, the sweeps, the recomputed residual, drift) over one
 synthetic system of the configuration's shape (BASELINE.json configs; seeded
@@ -380,7 +383,8 @@ def run_ours(args, cfg, rank, world, dev):
     import paper_2104_12570_b200 as pb
     from paper_2104_12570_b200 import _lib
     from paper_2104_12570_b200.bak import _Workspace, _ptr, _stream_ptr, _workspace_bytes
-    from paper_2104_12570_b200.sharded import DistComm, partition_rows, solve_bak_rowsharded
+    from paper_2104_12570_b200.sharded import (DistComm, partition_rows, partition_systems,
+                                               solve_bak_batched_sharded, solve_bak_rowsharded)
 
     lib = _lib.load()
     torch.cuda.set_device(dev)
@@ -392,8 +396,7 @@ def run_ours(args, cfg, rank, world, dev):
     force_shard = os.environ.get("BAK_FORCE_SHARDED") == "1"  # exercise the N>1 code path at N=1 (NCCL, 1 rank)
     sharded_rows = (not batched) and (world > 1 or force_shard)
     if batched:
-        per = -(-cfg["nsys"] // world)
-        s0, s1 = min(cfg["nsys"], rank * per), min(cfg["nsys"], (rank + 1) * per)
+        s0, s1 = partition_systems(cfg["nsys"], world, rank)
         dm, y = make_inputs(cfg, dev, seed=1234 + rank, nsys=s1 - s0)
         local_units = dm.nsys
     elif sharded_rows:
@@ -407,8 +410,8 @@ def run_ours(args, cfg, rank, world, dev):
     comm = DistComm() if (world > 1 or force_shard) else None
 
     def step(v=variant):
-        if batched:
-            return pb.solve_bak_batched(dm, y, scfg, return_device=True)
+        if batched:  # this rank's systems; no communication on the data path
+            return solve_bak_batched_sharded(dm, y, scfg, comm, local=True, return_device=True)[2]
         if cfg.get("thr"):
             return pb.solve_bakp(dm, y, pb.BlockConfig(base=scfg, thr=cfg["thr"]), variant=v, return_device=True)
         if sharded_rows:
@@ -487,14 +490,17 @@ def run_ours(args, cfg, rank, world, dev):
         sqpart = torch.zeros(nblk, dtype=torch.float64, device=dev)
         delta = torch.full((dm.vars,), 1e-3, dtype=torch.float64, device=dev)
         ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
+        pstat = torch.zeros(4, dtype=torch.int64, device=dev)
         e = y.clone()
         st = _stream_ptr(torch, dev)
 
         def one_pass():
             _lib.check(lib.bak_gram_pass(code, dm.ptr, dm.obs, dm.vars, dm.ldx, _ptr(e), _ptr(delta), 1, 1,
-                                         _ptr(gpart), _ptr(sqpart), _ptr(ctrl), st), "bak_gram_pass")
+                                         _ptr(gpart), _ptr(sqpart), _ptr(ctrl), _ptr(pstat), st), "bak_gram_pass")
         one_pass()
         k_ms, _ = _timed(one_pass, max(3, args.steps), dev, 1)
+        if int(pstat[2].item()):
+            raise RuntimeError(f"bak_gram_pass device error {int(pstat[2].item())}")
         k_ms /= max(3, args.steps)
         k_sweeps = 1
         alg_bytes = xbytes
@@ -721,7 +727,15 @@ def main():
     ap.add_argument("--no-exact", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    # --gpus N > 1 outside a launcher: re-run this script as N ranks (one per
+    # GPU) under torch.distributed.run; rank 0's JSON line goes to our stdout
+    from paper_2104_12570_b200 import launch
+    rc = launch.relaunch_if_needed(args.gpus, os.path.abspath(__file__), sys.argv[1:], stdout=json_fd)
+    if rc is not None:
+        sys.exit(rc)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch

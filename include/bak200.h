@@ -123,13 +123,16 @@ int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t
 int64_t bak_gram_dot_rows(int dtype, int64_t obs, int64_t vars);
 int bak_gram_matrix_dot(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
                         const void* e, double* g0, void* workspace, int64_t workspace_bytes, void* stream);
+/* status (int64[4] as bak_sweep, may be NULL): a pipeline wait past its
+ * deadline sets status[2] = BAK_ETIMEOUT (the pass results are then invalid). */
 int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                   const double* delta, int apply, int dot, double* gpart, double* sqpart,
-                  const int64_t* done_flag, void* stream);
+                  const int64_t* done_flag, int64_t* status, void* stream);
 /* bak_gram_pass + (afin != NULL) resid = y - x @ afin fused into the same pass. */
 int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                         const double* delta, int apply, int dot, double* gpart, double* sqpart,
-                        const int64_t* done_flag, const void* afin, const void* y, void* resid, void* stream);
+                        const int64_t* done_flag, const void* afin, const void* y, void* resid,
+                        int64_t* status, void* stream);
 int bak_gram_solve(int dtype, int64_t vars, const double* gpart, const double* sqpart, int64_t nparts,
                    int64_t sweep, int64_t max_iter, double thresh2, const int32_t* cols, int64_t ncols,
                    int64_t cols_stride, const void* norms2, const double* G, void* a, double* delta,
@@ -197,6 +200,9 @@ int bak_copy_rows_h2d(void* dst, int64_t dld, const void* src, int64_t sld, int6
  * allocation and peers map its base address. */
 int bak_dev_alloc(int64_t bytes, void** devptr);
 int bak_dev_free(void* devptr);
+/* Zero `bytes` of a bak_dev_alloc allocation (synchronous; used when the
+ * row-shard epoch count restarts before it would wrap 31 bits). */
+int bak_dev_zero(void* devptr, int64_t bytes);
 int bak_ipc_get_handle(void* devptr, void* handle64);
 int bak_ipc_open_handle(const void* handle64, void** devptr);
 int bak_ipc_close(void* devptr);

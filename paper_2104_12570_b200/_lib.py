@@ -56,9 +56,9 @@ SIGNATURES = {
     "bak_score_columns": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_block_deltas": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bak_gram_matrix_dot": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
-    "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
+    "bak_gram_pass": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "bak_gram_pass_resid": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,
-                                   _vp, _vp]),
+                                   _vp, _vp, _vp]),
     "bak_copy_rows_h2d": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp]),
     "bak_gram_solve": (_int, [_int, _i64, _vp, _vp, _i64, _i64, _i64, _dbl, _vp, _i64, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp]),
@@ -69,6 +69,7 @@ SIGNATURES = {
                                   _vp, _i64, _int, _vp, _i64, _vp]),
     "bak_dev_alloc": (_int, [_i64, ctypes.POINTER(_vp)]),
     "bak_dev_free": (_int, [_vp]),
+    "bak_dev_zero": (_int, [_vp, _i64]),
     "bak_ipc_get_handle": (_int, [_vp, _vp]),
     "bak_ipc_open_handle": (_int, [_vp, ctypes.POINTER(_vp)]),
     "bak_ipc_close": (_int, [_vp]),

@@ -154,7 +154,10 @@ def to_device_matrix(x, device=None):
         itemsize = 8 if np_dtype == np.float64 else 4
         ld = _aligned_ld(obs, itemsize)
         if (x.is_cuda and x.stride(0) == 1 and x.stride(1) >= obs and (x.stride(1) * itemsize) % 16 == 0
-                and x.data_ptr() % 16 == 0 and x.device == dev):
+                and x.data_ptr() % 16 == 0 and x.device == dev
+                and x.storage_offset() + nv * x.stride(1) <= x.untyped_storage().nbytes() // itemsize):
+            # (the padded (vars, ld) view covers ld elements of the last column: only when they are
+            # inside the storage, e.g. not for a row-offset slice of a larger column-major matrix)
             # zero-copy view of an existing column-major device matrix
             data = torch.as_strided(x, (nv, x.stride(1)), (x.stride(1), 1))
             return DeviceMatrix(data, obs, nv, np_dtype)
@@ -251,6 +254,37 @@ def _permutation_chunks(seed, nvars, nz_mask):
         yield order[nz_mask[order]] if nz_mask is not None else order.copy()
 
 
+# "auto" for systems whose residual does not fit on chip: the exact kernel then
+# streams e, x_j and x_{j+1} per column (~4 column-lengths of HBM traffic per
+# column of x), the GRAM sweep reads x once per sweep after one G = X^T X
+# (~8.5 passes' worth for 2^24 x 256 fp64).  GRAM meets the same parity bar
+# (tests/test_fullsize_reference_gpu.py) and is reported as variant "gram".
+_AUTO_GRAM_MAX_VARS = 256
+_AUTO_GRAM_MIN_SWEEPS = 4
+
+
+def _auto_variant(lib, x, cfg):
+    """Variant "auto" resolves to: the exact on-chip kernels (CTA / cluster /
+    grid) when the residual fits on chip; else GRAM when vars <= 256 and at
+    least 4 sweeps are allowed; else the exact STREAM kernel."""
+    if isinstance(x, DeviceMatrix):
+        obs, nv, code = x.obs, x.vars, x.code
+    else:
+        shape = getattr(x, "shape", None)
+        if shape is None or len(shape) != 2:
+            return "auto"  # coerced (and rejected if not 2-d) by to_device_matrix
+        obs, nv = int(shape[0]), int(shape[1])
+        dt = str(getattr(x, "dtype", "float64"))
+        code = _lib.F32 if dt.endswith("float32") else _lib.F64
+    if obs < 1 or nv < 1:
+        return "auto"
+    picked = int(lib.bak_sweep_pick_variant(code, obs, nv))
+    if (picked == _lib.VARIANTS["stream"] and nv <= _AUTO_GRAM_MAX_VARS
+            and cfg.max_iter >= _AUTO_GRAM_MIN_SWEEPS):
+        return "gram"
+    return "auto"
+
+
 def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto", device=None,
               return_device=False) -> SolveReport:
     """Solve min ||y - x a|| by repeated single-column updates on the GPU.
@@ -265,6 +299,8 @@ def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto
     lib = _lib.load()
     if variant not in _lib.VARIANTS:
         raise ValueError(f"unknown variant {variant!r}, expected one of {tuple(_lib.VARIANTS)}")
+    if variant == "auto":
+        variant = _auto_variant(lib, x, cfg)
     if variant == "gram" and _pipelinable(torch, x):
         return _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device)
     dm = to_device_matrix(x, device)
@@ -445,6 +481,11 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
     yd = _to_device_vector(y, np_dtype, dev)
     if yd.shape[0] != obs:
         raise ValueError(f"y has length {yd.shape[0]}, expected {obs}")
+    a0d = None
+    if a0 is not None:  # validated before any copy is queued
+        a0d = _to_device_vector(a0, np_dtype, dev, "a0").clone()
+        if a0d.shape[0] != nv:
+            raise ValueError(f"a0 has length {a0d.shape[0]}, expected {nv}")
     main = torch.cuda.current_stream(dev)
     st = ctypes.c_void_p(main.cuda_stream)
     t0 = time.perf_counter()
@@ -454,6 +495,10 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
     copy_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     for cs in copy_streams:
         cs.wait_stream(main)
+        # the copies write `data` on these streams: on ANY exit (an exception
+        # included) the caching allocator must not hand the block out again
+        # before they are done
+        data.record_stream(cs)
     events = []
     for i, (r0, r1) in enumerate(blocks):
         cs = copy_streams[i % 2]
@@ -473,11 +518,7 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
         r_z = torch.zeros(obs, dtype=yd.dtype, device=dev)
         return SolveReport(a_z if return_device else a_z.cpu().numpy(), r_z if return_device else r_z.cpu().numpy(),
                            [] if cfg.record_history else None, 0, True, time.perf_counter() - t0)
-    a = torch.zeros(nv, dtype=yd.dtype, device=dev)
-    if a0 is not None:
-        a = _to_device_vector(a0, np_dtype, dev, "a0").clone()
-        if a.shape[0] != nv:
-            raise ValueError(f"a0 has length {a.shape[0]}, expected {nv}")
+    a = a0d if a0d is not None else torch.zeros(nv, dtype=yd.dtype, device=dev)
     thresh2 = cfg.tol * cfg.tol * ynorm2 if cfg.tol > 0 else -1.0
     e = yd.clone()
     nblk = lib.bak_gram_pass_blocks(code, nv)
@@ -528,7 +569,8 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
         afin = a if (last and fused) else None
         _lib.check(lib.bak_gram_pass_resid(code, dm.ptr, obs, nv, ld, _ptr(e), _ptr(delta), 1, dot, _ptr(gpart),
                                            _ptr(sqpart), _ptr(ctrl), _ptr(afin), _ptr(yd if afin is not None else None),
-                                           _ptr(resid if afin is not None else None), st), "bak_gram_pass")
+                                           _ptr(resid if afin is not None else None), _ptr(status), st),
+                   "bak_gram_pass")
 
     gp, sp = gp0.reshape(-1), sp0.reshape(-1)
     for sweep in range(1, cfg.max_iter + 1):
@@ -539,6 +581,8 @@ def _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device):
             break
     solve(gp, sp, cfg.max_iter + 1)
     stat = status.cpu().numpy()
+    if int(stat[2]):
+        raise _lib.BakError(f"GRAM device error {int(stat[2])} (3 = pipeline timeout)")
     sweeps, converged = int(stat[0]), bool(stat[1])
     if not fused:
         _residual(lib, dm, a, yd, resid, ws, st)

@@ -434,7 +434,7 @@ static int launch_gram_impl(int dtype, const SweepParams& prm, int64_t vars, voi
   auto pass = [&](int apply, int dot) -> int {
     if (use_tma)
       return launch_gram_pass_tma(dtype, prm.x, prm.obs, prm.ldx, vars, prm.e, delta, apply, dot, gpart, sqpart,
-                                  &ctrl->done, st);
+                                  &ctrl->done, st, nullptr, nullptr, nullptr, prm.status);
     pp.apply = apply;
     pp.dot = dot;
     if (dtype == BAK_F64)
@@ -541,19 +541,19 @@ extern "C" int bak_gram_matrix_dot(int dtype, const void* x, int64_t obs, int64_
 extern "C" int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                                    const double* delta, int apply, int dot, double* gpart, double* sqpart,
                                    const int64_t* done_flag, const void* afin, const void* y, void* resid,
-                                   void* stream);
+                                   int64_t* status, void* stream);
 
 extern "C" int bak_gram_pass(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                              const double* delta, int apply, int dot, double* gpart, double* sqpart,
-                             const int64_t* done_flag, void* stream) {
+                             const int64_t* done_flag, int64_t* status, void* stream) {
   return bak_gram_pass_resid(dtype, x, obs, vars, ldx, e, delta, apply, dot, gpart, sqpart, done_flag, nullptr,
-                             nullptr, nullptr, stream);
+                             nullptr, nullptr, status, stream);
 }
 
 extern "C" int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, void* e,
                                    const double* delta, int apply, int dot, double* gpart, double* sqpart,
                                    const int64_t* done_flag, const void* afin, const void* y, void* resid,
-                                   void* stream) {
+                                   int64_t* status, void* stream) {
   if ((dtype != BAK_F32 && dtype != BAK_F64) || obs < 1 || !gram_supported(vars) || ldx < obs || !x || !e ||
       !delta || !gpart || !sqpart || !done_flag || (afin && (!y || !resid))) {
     set_error("bak_gram_pass: bad arguments");
@@ -562,7 +562,7 @@ extern "C" int bak_gram_pass_resid(int dtype, const void* x, int64_t obs, int64_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (gram_tma_supported(vars))
     return launch_gram_pass_tma(dtype, x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart, done_flag, st, afin,
-                                y, resid);
+                                y, resid, status);
   if (afin) {
     set_error("bak_gram_pass: fused residual needs the TMA pass (vars <= 256)");
     return BAK_EUNSUPPORTED;
@@ -664,7 +664,7 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
   auto pass = [&](int apply, int dot, bool final_pass) -> int {
     if (use_tma)
       return launch_gram_pass_tma(dtype, x, obs, ldx, vars, e, delta, apply, dot, gpart, sqpart, &ctrl->done, st,
-                                  final_pass && fuse_resid ? a : nullptr, y, resid);
+                                  final_pass && fuse_resid ? a : nullptr, y, resid, status);
     pp.apply = apply;
     pp.dot = dot;
     if (dtype == BAK_F64)

@@ -35,6 +35,7 @@ struct TmaPassParams {
   const void* afin;  // non-null: also write resid = y - x @ afin (fused final residual, bak.py:130)
   const void* y;
   void* resid;
+  int64_t* status;  // non-null: a spin wait past its deadline reports BAK_ETIMEOUT in status[2]
 };
 
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -104,7 +105,10 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
         if (u >= kS) {
           const uint64_t t0 = globaltimer();
           while (!mbar_test(&empty[s], ph ^ 1u))
-            if (globaltimer() - t0 > kTimeoutNs) return;
+            if (globaltimer() - t0 > kTimeoutNs) {
+              report_error(p.status, BAK_ETIMEOUT);
+              return;
+            }
         }
         mbar_arrive_expect_tx(&full[s], kTileBytes);
         tma_2d(xs + static_cast<size_t>(s) * KR * VB, &xmap, static_cast<int>(tile * KR), 0, &full[s]);
@@ -122,6 +126,10 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
   int s = 0;
   uint32_t ph = 0;
   int64_t tile = blockIdx.x;
+  // After a timed-out wait the warp stops waiting (it keeps the named-barrier
+  // schedule of the other warps, so nothing hangs) and the error is reported:
+  // the results of this launch are garbage and the caller raises.
+  bool timed_out = false;
   // fp32 sweep passes (apply + dot, no fused residual): x is read from shared
   // memory once per element into registers; (X d)_r runs as fp32 FMAs over the
   // warp's columns, and each column's two products of a lane (rows r, r+32)
@@ -157,10 +165,14 @@ __global__ void __launch_bounds__(kCons + 32, 1) gram_pass_tma_kernel(const __gr
         if (want_r) y_next[i] = nok ? yv[nrow] : T(0);
       }
     }
-    {
+    if (!timed_out) {
       const uint64_t t0 = globaltimer();
       while (!mbar_test(&full[s], ph))
-        if (globaltimer() - t0 > kTimeoutNs) break;
+        if (globaltimer() - t0 > kTimeoutNs) {
+          timed_out = true;
+          report_error(p.status, BAK_ETIMEOUT);
+          break;
+        }
     }
     const T* X = xs + static_cast<size_t>(s) * KR * VB + static_cast<size_t>(warp) * CW * KR + lane;
     float xr[kF32 ? RPL : 1][kF32 ? CW : 1];
@@ -298,7 +310,7 @@ int gram_tma_grid(int dtype) {
 // x: column-major obs x vars, ldx*sizeof(T) % 16 == 0
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
                          const double* delta, int apply, int dot, double* gpart, double* sqpart, const int64_t* done,
-                         cudaStream_t st, const void* afin, const void* y, void* resid) {
+                         cudaStream_t st, const void* afin, const void* y, void* resid, int64_t* status) {
   auto enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -320,7 +332,7 @@ int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int
     set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
     return BAK_ECUDA;
   }
-  TmaPassParams p{obs, vars, (obs + kr - 1) / kr, e, delta, apply, dot, gpart, sqpart, done, afin, y, resid};
+  TmaPassParams p{obs, vars, (obs + kr - 1) / kr, e, delta, apply, dot, gpart, sqpart, done, afin, y, resid, status};
   const int grid = gram_tma_grid(dtype);
   if (dtype == BAK_F64) {
     if (cw == 8) return launch_cw<double, 8>(map, p, grid, st);

@@ -11,7 +11,8 @@
 //   - every CTA polls its own rank's mailbox (local memory) for the N records
 //     and sums them in RANK ORDER, so d_j and a are bit-identical on all ranks.
 // Epochs are unique per call (epoch_base + reduction index), so mailboxes are
-// never reset between columns or calls.  Every spin wait has a deadline; a
+// not reset between columns or calls; the host restarts the count (after
+// zeroing every mailbox between two barriers) before it would wrap 31 bits.  Every spin wait has a deadline; a
 // missing rank surfaces as BAK_ETIMEOUT, not a hang.
 //
 // Emulation (nranks_local = N > 1, one device): the grid is N groups of CTAs,
@@ -385,6 +386,17 @@ extern "C" int bak_dev_alloc(int64_t bytes, void** devptr) {
 
 extern "C" int bak_dev_free(void* devptr) {
   BAK_CHECK_CUDA(cudaFree(devptr));
+  return BAK_OK;
+}
+
+// Zero a mailbox before its epoch count restarts (synchronous).
+extern "C" int bak_dev_zero(void* devptr, int64_t bytes) {
+  if (!devptr || bytes < 1) {
+    set_error("bak_dev_zero: bad arguments");
+    return BAK_EINVAL;
+  }
+  BAK_CHECK_CUDA(cudaMemset(devptr, 0, static_cast<size_t>(bytes)));
+  BAK_CHECK_CUDA(cudaDeviceSynchronize());
   return BAK_OK;
 }
 

@@ -787,7 +787,7 @@ static bool plan_env(int dtype, int variant, int64_t obs, SweepPlan& pl) {
   return plan_fill(dtype, variant, obs, nt, e, parts, pl, 2);
 }
 
-bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
+bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl, bool force_flat) {
   const int sms = device_sms();
   if (plan_env(dtype, variant, obs, pl)) return true;
   // Measured on B200 (tools/tune2.sh): E = 8 rows per thread and as few warps
@@ -821,7 +821,7 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl) {
     // evenly over a multiple of kGridCluster CTAs.  BAK_GRID_FLAT=1: one level.
     const char* flat = getenv("BAK_GRID_FLAT");
     const int max_parts = kGridCluster * (grid_cluster_capacity() < 32 ? grid_cluster_capacity() : 32);
-    if (!(flat && flat[0] == '1') && coop_clusters_ok()) {
+    if (!force_flat && !(flat && flat[0] == '1') && coop_clusters_ok()) {
       for (int e : kEs) {
         const int64_t rows = 256LL * e;
         const int64_t parts = round_up((obs + rows - 1) / rows, kGridCluster);
@@ -860,9 +860,7 @@ int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm, cudaSt
     // clusters did not fit co-resident: one-level grid exchange
     if (getenv("BAK_DEBUG")) fprintf(stderr, "bak: two-level grid exchange unavailable (%s)\n", bak_last_error());
     SweepPlan flat;
-    setenv("BAK_GRID_FLAT", "1", 0);
-    const bool ok = plan_onchip(dtype, BAK_VARIANT_GRID, prm.obs, flat);
-    unsetenv("BAK_GRID_FLAT");
+    const bool ok = plan_onchip(dtype, BAK_VARIANT_GRID, prm.obs, flat, /*force_flat=*/true);
     if (!ok) return rc;
     g_err_clear();
     SweepParams p2 = prm;

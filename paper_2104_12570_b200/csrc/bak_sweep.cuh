@@ -41,7 +41,8 @@ struct SweepPlan {
   int cluster = 0;  // GRID: CTAs per cluster of the two-level exchange (0 = one level)
 };
 
-bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl);
+// force_flat: GRID plans use the one-level exchange (as BAK_GRID_FLAT=1)
+bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl, bool force_flat = false);
 int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm, cudaStream_t st);
 
 // e streamed through HBM (tall systems past on-chip capacity)
@@ -64,7 +65,8 @@ bool gram_tma_supported(int64_t vars);
 int gram_tma_grid(int dtype);
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,
                          const double* delta, int apply, int dot, double* gpart, double* sqpart, const int64_t* done,
-                         cudaStream_t st, const void* afin = nullptr, const void* y = nullptr, void* resid = nullptr);
+                         cudaStream_t st, const void* afin = nullptr, const void* y = nullptr, void* resid = nullptr,
+                         int64_t* status = nullptr);
 int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st);
 
 }  // namespace bak

@@ -39,6 +39,83 @@ def partition_rows(obs, world, rank, align=2):
     return r0, r1
 
 
+def partition_systems(nsys, world, rank):
+    """Contiguous, balanced system range [s0, s1) of `rank` (sizes differ by at most one)."""
+    base, extra = divmod(int(nsys), int(world))
+    s0 = rank * base + min(rank, extra)
+    return s0, s0 + base + (1 if rank < extra else 0)
+
+
+def solve_bak_batched_sharded(xs, ys, config: SolveConfig | None = None, comm=None, *, local=False, gather=False,
+                              device=None, return_device=False):
+    """Many independent systems sharded over ranks with NO communication on the
+    data path (north-star (5)): rank r solves the systems
+    ``partition_systems(nsys, world, r)`` with ``solve_bak_batched`` (one CTA
+    per system) on its own GPU — the reference's equivalent is a loop of
+    ``solve_bak`` (bak.py:146) over the systems, which shards trivially.
+
+    xs / ys: the whole batch (``local=False``: each rank takes its slice; host
+    arrays are sliced without copying) or this rank's shard (``local=True``).
+    Returns ``(s0, s1, BatchSolveReport)`` for the rank's systems (s0, s1 are
+    None for a local shard without gather: no exchange tells the offset); with
+    ``gather=True`` the per-system coefficients, sweeps and flags of ALL ranks
+    are all-gathered once at the end (after the solves) and the report covers
+    the whole batch (residuals stay per rank: ``residual`` is None).
+    """
+    from .bak import BatchSolveReport, solve_bak_batched
+    world = getattr(comm, "world", 1) if comm is not None else 1
+    rank = getattr(comm, "rank", 0) if comm is not None else 0
+    def _n(b):
+        return int(b.nsys) if hasattr(b, "nsys") else int(b.shape[0])
+
+    if local:
+        nloc = _n(xs)
+        counts = [nloc]
+        if comm is not None and world > 1 and gather:
+            torch = _torch()
+            dev = device or torch.device("cuda", torch.cuda.current_device())
+            counts = [int(c.item()) for c in comm.all_gather([torch.tensor([nloc], dtype=torch.int64, device=dev)])]
+        # global offsets are known only after the count exchange (gather=True)
+        s0 = sum(counts[:rank]) if len(counts) == world else None
+        s1 = s0 + nloc if s0 is not None else None
+        xl, yl = xs, ys
+    else:
+        nsys = _n(xs)
+        s0, s1 = partition_systems(nsys, world, rank)
+        xl, yl = xs[s0:s1], ys[s0:s1]
+    rep = solve_bak_batched(xl, yl, config, device=device, return_device=True)
+    if not gather or comm is None or world == 1:
+        if not return_device:
+            rep = BatchSolveReport(_host(rep.a_hat), _host(rep.residual),
+                                   None if rep.residual_norm_history is None else _host(rep.residual_norm_history),
+                                   rep.sweeps_run, rep.converged, rep.wall_time, rep.drift_warning)
+        return s0, s1, rep
+    torch = _torch()
+    dev = rep.a_hat.device
+    # one collective after all the work: pad every rank's block to the largest
+    sizes = ([partition_systems(_n(xs), world, r) for r in range(world)] if not local
+             else [(sum(counts[:r]), sum(counts[: r + 1])) for r in range(world)])
+    nmax = max(b - a for a, b in sizes)
+    nv = rep.a_hat.shape[1]
+
+    def pad(t, width):
+        out = torch.zeros((nmax, width), dtype=t.dtype, device=dev)
+        out[: t.shape[0]] = t.reshape(t.shape[0], width)
+        return out
+
+    flags = torch.stack([torch.as_tensor(rep.sweeps_run, dtype=torch.float64, device=dev),
+                         torch.as_tensor(rep.converged, dtype=torch.float64, device=dev),
+                         torch.as_tensor(rep.drift_warning, dtype=torch.float64, device=dev)], dim=1)
+    ga = comm.all_gather([pad(rep.a_hat, nv)])
+    gf = comm.all_gather([pad(flags, 3)])
+    a_all = torch.cat([ga[r][: b - a] for r, (a, b) in enumerate(sizes)])
+    f_all = torch.cat([gf[r][: b - a] for r, (a, b) in enumerate(sizes)]).cpu().numpy()
+    out = BatchSolveReport(a_all if return_device else _host(a_all), None, None,
+                           f_all[:, 0].astype(np.int64), f_all[:, 1].astype(bool), rep.wall_time,
+                           f_all[:, 2].astype(bool))
+    return 0, a_all.shape[0], out
+
+
 def rank_order_sum(tensors):
     """Elementwise sum in rank order (fixed, identical on every rank)."""
     out = tensors[0].clone()
@@ -57,6 +134,9 @@ class LocalComm:
         assert len(per_rank) == self.world
         return list(per_rank)
 
+    def barrier(self):
+        pass
+
 
 class DistComm:
     """One rank per process over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
@@ -67,6 +147,9 @@ class DistComm:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
 
     def all_gather(self, per_rank):
         assert len(per_rank) == 1
@@ -172,6 +255,8 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
         rank = getattr(comm, "rank", 0)
         mb = getattr(comm, "_bak_mailboxes", None)
         if mb is None or mb.nranks != world:
+            if mb is not None:
+                mb.close()  # release the replaced mailbox and its peer mappings
             mb = Mailboxes(world, comm if world > 1 else None, dev)
             try:
                 comm._bak_mailboxes = mb
@@ -230,7 +315,8 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
             _lib.check(lib.bak_gram_pass_resid(code, s.dm.ptr, s.dm.obs, nv, s.dm.ldx, _ptr(s.e), _ptr(delta), apply,
                                                dot, _ptr(s.gpart), _ptr(s.sqpart), _ptr(ctrl),
                                                _ptr(a if fin else None), _ptr(s.y if fin else None),
-                                               _ptr(s.resid if fin else None), st), "bak_gram_pass")
+                                               _ptr(s.resid if fin else None), _ptr(status), st),
+                       "bak_gram_pass")
         gp = comm.all_gather([s.gpart for s in shards])
         sp = comm.all_gather([s.sqpart for s in shards])
         return torch.cat([g.reshape(-1) for g in gp]), torch.cat(sp)
@@ -249,6 +335,8 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
             break
     solve(gp, sp, cfg.max_iter + 1)
     stat = status.cpu().numpy()
+    if int(stat[2]):
+        raise _lib.BakError(f"GRAM row-shard device error {int(stat[2])} (3 = pipeline timeout)")
     sweeps, converged = int(stat[0]), bool(stat[1])
 
     return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "gram-rowshard",
@@ -297,15 +385,24 @@ class Mailboxes:
     DistComm: each rank allocates its mailbox, exports a CUDA IPC handle, the
     handles are all-gathered and every rank maps its peers' mailboxes (NVLink
     peer memory).  local=N: N emulated ranks share one device buffer.
-    Epochs only ever increase (``next_epochs``) so mailboxes are never reset.
+    Epochs increase from call to call (``next_epochs``), so a record left by an
+    earlier call never matches a later one.  The kernel tags records with 31
+    bits; before the counter would wrap, every rank zeroes its own mailbox
+    between two collective barriers and the count restarts at 0 (every rank
+    calls ``next_epochs`` with the same counts, so they all reset together).
     """
+
+    EPOCH_LIMIT = 0x7FFFFFFF
 
     def __init__(self, nranks, comm=None, device=None):
         torch = _torch()
         lib = _lib.load()
         self.nranks = nranks
         self.epoch = 0
+        self._own = None
+        self._comm = None if (comm is None or isinstance(comm, LocalComm)) else comm
         per = int(lib.bak_mailbox_bytes(nranks))
+        self._per = per
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self._opened = []
         if comm is None or isinstance(comm, LocalComm):
@@ -335,18 +432,46 @@ class Mailboxes:
         self.array = (ctypes.c_void_p * nranks)(*self.ptrs)
 
     def next_epochs(self, count):
+        """Reserve ``count`` epochs (tags base+1 .. base+count) for one call."""
+        if count + 2 >= self.EPOCH_LIMIT:
+            raise ValueError(f"one row-sharded call needs {count} exchange epochs (> 2^31)")
+        if self.epoch + count + 2 >= self.EPOCH_LIMIT:
+            self.reset()
         base = self.epoch
-        self.epoch = (self.epoch + count + 2) & 0x7FFFFFFF
+        self.epoch += count + 2
         return base
 
-    def close(self):
+    def reset(self):
+        """Zero the mailboxes and restart the epoch count (collective over the ranks)."""
+        torch = _torch()
         lib = _lib.load()
-        for p in self._opened:
+        torch.cuda.synchronize()  # no kernel of this rank still reads or writes a mailbox
+        if self._comm is not None:
+            self._comm.barrier()  # ... nor one of a peer
+        if self.buf is not None:
+            self.buf.zero_()
+        else:
+            _lib.check(lib.bak_dev_zero(ctypes.c_void_p(self._own), self._per), "bak_dev_zero")
+        torch.cuda.synchronize()
+        if self._comm is not None:
+            self._comm.barrier()  # every mailbox is zero before any rank posts again
+        self.epoch = 0
+
+    def close(self):
+        """Unmap the peers' mailboxes and free this rank's (idempotent)."""
+        try:
+            lib = _lib.load()
+        except Exception:  # interpreter shutdown
+            return
+        for p in getattr(self, "_opened", ()):
             lib.bak_ipc_close(ctypes.c_void_p(p))
         self._opened = []
         if getattr(self, "_own", None):
             lib.bak_dev_free(ctypes.c_void_p(self._own))
             self._own = None
+
+    def __del__(self):
+        self.close()
 
 
 def sweep_rowshard(dm, e, a, norms, max_iter, thresh2, mailboxes, rank, nranks, nranks_local=1, history=None,

@@ -12,7 +12,14 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_", "select_", "matio_")))
+                  if not os.path.basename(p).startswith(("kat_coordinate", "kat_block_deltas", "bakp_", "select_", "matio_",
+                                                          "fullsize_")))
+
+
+def fullsize(name):
+    """Full-size reference outputs (make_golden_fullsize.py): dict of arrays."""
+    with np.load(os.path.join(GOLDEN, f"fullsize_{name}.npz"), allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}
 
 
 def bakp_names():

@@ -82,6 +82,14 @@ TF32_MMA_PEAK_TFLOPS = 277.6  # measured legacy tf32 mma.sync ceiling (tools/mic
 REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -521,15 +529,25 @@ def run_ours(args, cfg, rank, world, dev):
             gk, gbound, gpeak = ("gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
                                  "tensor (fp64 DMMA)", DMMA_PEAK_TFLOPS)
             gsrc = "tools/micro/dmma_peak.cu: register-only m8n8k4 f64 DMMA, all SMs, 1965 MHz"
-        else:  # fp32: 3xTF32, three tf32 products per pair; diagonal blocks 20 of 32 16x8 tiles
+        elif os.environ.get("BAK_GRAM_G", "")[:1] in ("x", "d"):  # legacy mma.sync 3xTF32 kernel
             flops = 3 * 2.0 * dm.obs * (4096 * noff + 2560 * nb)
             gk, gbound, gpeak = ("gram_dmma_kernel<float, X3> (3xTF32 mma.sync m16n8k8, fp64 totals)",
                                  "tensor (tf32 mma.sync)", TF32_MMA_PEAK_TFLOPS)
             gsrc = "tools/micro/tf32_peak.cu: register-only m16n8k8 tf32 mma.sync, all SMs"
+        else:  # fp32: tcgen05 kind::tf32, two products (Hi^T Hi + Hi^T 2Lo) over the full vb x vb S
+            vb = 128 if dm.vars <= 128 else 256
+            flops = 2 * 2.0 * dm.obs * vb * vb
+            gk, gbound = ("gram_tc_kernel (tcgen05.mma kind::tf32 M128 N%d, TMEM accumulators, TMA 128B-swizzle "
+                          "ring; hi/lo split + fp64 norms and x^T e on the CUDA cores)" % vb,
+                          "tensor (tcgen05 tf32)")
+            gpeak = round(_peaks().get("bf16_tflops", 1665.7) / 2, 1)
+            gsrc = ("dense tf32 = 1/2 of the measured cuBLAS bf16 burst peak in MEASURED_PEAKS.json "
+                    "(tf32 issues at half the bf16 rate)")
         extra["gram_matrix"] = {"kernel": gk, "ms": round(g_ms, 3),
                                 "tflops_issued": round(flops / (g_ms / 1e3) / 1e12, 2),
                                 "bound": gbound, "peak_tflops": gpeak,
-                                "peak_source": gsrc + " (no such figure in MEASURED_PEAKS.json)",
+                                "peak_source": gsrc if "MEASURED_PEAKS" in gsrc
+                                else gsrc + " (no such figure in MEASURED_PEAKS.json)",
                                 "frac": round(flops / (g_ms / 1e3) / 1e12 / gpeak, 3),
                                 "share_of_step": round(g_ms / (ms / args.steps), 3)}
     elif cfg.get("thr"):

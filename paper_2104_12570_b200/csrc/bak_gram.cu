@@ -338,10 +338,10 @@ __global__ void __launch_bounds__(512, 1) gram_solve_kernel(const SolveParams p)
 static int64_t gram_nblk() { return 2 * static_cast<int64_t>(device_sms()); }
 
 // rows of gpart: the pass partials, or the fused first-sweep partials of the G kernel
-static int64_t gram_gpart_rows(int64_t obs, int64_t vars) {
+static int64_t gram_gpart_rows(int dtype, int64_t obs, int64_t vars) {
   int g0rows;
   int64_t chunk;
-  gram_g_workspace(obs, vars, g0rows, chunk);
+  gram_g_workspace(dtype, obs, vars, g0rows, chunk);
   return g0rows > gram_nblk() ? g0rows : gram_nblk();
 }
 
@@ -349,13 +349,13 @@ int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars) {
   (void)dtype;
   int64_t b = 0;
   b += vars * vars * 8;
-  b += gram_gpart_rows(obs, vars) * vars * 8;
+  b += gram_gpart_rows(dtype, obs, vars) * vars * 8;
   b += gram_nblk() * 8;
   b += vars * 8;
   b += 64;
   int nchunks;
   int64_t chunk;
-  b += gram_g_workspace(obs, vars, nchunks, chunk) + 256;
+  b += gram_g_workspace(dtype, obs, vars, nchunks, chunk) + 256;
   return round_up(b, 256) + 4096;
 }
 
@@ -408,7 +408,7 @@ static int launch_gram_impl(int dtype, const SweepParams& prm, int64_t vars, voi
   double* G = reinterpret_cast<double*>(w);
   w += vars * vars * 8;
   double* gpart = reinterpret_cast<double*>(w);
-  w += gram_gpart_rows(prm.obs, vars) * vars * 8;
+  w += gram_gpart_rows(dtype, prm.obs, vars) * vars * 8;
   double* sqpart = reinterpret_cast<double*>(w);
   w += nblk * 8;
   double* delta = reinterpret_cast<double*>(w);
@@ -460,7 +460,7 @@ static int launch_gram_impl(int dtype, const SweepParams& prm, int64_t vars, voi
   if (fuse_g0) {
     int g0rows;
     int64_t chunk;
-    gram_g_workspace(prm.obs, vars, g0rows, chunk);
+    gram_g_workspace(dtype, prm.obs, vars, g0rows, chunk);
     sp.nblk = g0rows;
   } else if ((rc = pass(0, 1))) {
     return rc;
@@ -493,10 +493,9 @@ extern "C" int bak_gram_pass_blocks(int dtype, int64_t vars) {
 }
 
 extern "C" int64_t bak_gram_matrix_workspace(int dtype, int64_t obs, int64_t vars) {
-  (void)dtype;
   int nchunks;
   int64_t chunk;
-  return gram_g_workspace(obs, vars, nchunks, chunk) + 256;
+  return gram_g_workspace(dtype, obs, vars, nchunks, chunk) + 256;
 }
 
 extern "C" int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t vars, int64_t ldx, double* G,
@@ -514,10 +513,9 @@ extern "C" int bak_gram_matrix(int dtype, const void* x, int64_t obs, int64_t va
 }
 
 extern "C" int64_t bak_gram_dot_rows(int dtype, int64_t obs, int64_t vars) {
-  (void)dtype;
   int nchunks;
   int64_t chunk;
-  gram_g_workspace(obs, vars, nchunks, chunk);
+  gram_g_workspace(dtype, obs, vars, nchunks, chunk);
   return nchunks;
 }
 
@@ -627,7 +625,7 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
   double* G = reinterpret_cast<double*>(w);
   w += vars * vars * 8;
   double* gpart = reinterpret_cast<double*>(w);
-  w += gram_gpart_rows(obs, vars) * vars * 8;
+  w += gram_gpart_rows(dtype, obs, vars) * vars * 8;
   double* sqpart = reinterpret_cast<double*>(w);
   w += nblk * 8;
   double* delta = reinterpret_cast<double*>(w);
@@ -690,7 +688,7 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
   if (fuse_g0) {  // the first g came out of the G kernel
     int g0rows;
     int64_t chunk;
-    gram_g_workspace(obs, vars, g0rows, chunk);
+    gram_g_workspace(dtype, obs, vars, g0rows, chunk);
     sp.nblk = g0rows;
   } else if ((rc = pass(0, 1, false))) {
     return rc;

@@ -412,7 +412,12 @@ static GramSplit gram_split(int64_t obs, int64_t vars) {
   return g;
 }
 
-int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk) {
+int64_t gram_g_workspace(int dtype, int64_t obs, int64_t vars, int& nchunks, int64_t& chunk) {
+  if (gram_tc_enabled(dtype, vars)) {  // one reduced row of g0
+    nchunks = 1;
+    chunk = obs;
+    return gram_tc_workspace(obs, vars);
+  }
   const GramSplit g = gram_split(obs, vars);
   nchunks = g.cd;  // partial rows of the fused g0
   chunk = g.chunk_d;
@@ -422,9 +427,11 @@ int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk
 
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
                   int64_t part_bytes, cudaStream_t st, void* norms_out, const void* e, double* g0) {
+  if (gram_tc_enabled(dtype, vars))
+    return launch_gram_g_tc(x, obs, ldx, vars, G, part_ws, part_bytes, st, norms_out, e, g0, nullptr);
   int nchunks;
   int64_t chunk;
-  const int64_t need = gram_g_workspace(obs, vars, nchunks, chunk);
+  const int64_t need = gram_g_workspace(dtype, obs, vars, nchunks, chunk);
   if (part_bytes < need) {
     set_error("gram: partial workspace too small");
     return BAK_EWORKSPACE;

@@ -300,6 +300,8 @@ int launch_cw(const CUtensorMap& map, const TmaPassParams& p, int grid, cudaStre
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
+
 bool gram_tma_supported(int64_t vars) { return vars >= 1 && vars <= 256 && encode_fn() != nullptr; }
 
 int gram_tma_grid(int dtype) {

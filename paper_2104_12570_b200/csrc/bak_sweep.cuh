@@ -57,7 +57,14 @@ int launch_stream(int dtype, const StreamPlan& pl, const SweepParams& prm, cudaS
 // GRAM variant (algebraically equivalent sweep through G = X^T X)
 int64_t gram_workspace_bytes(int dtype, int64_t obs, int64_t vars);
 bool gram_supported(int64_t vars);
-int64_t gram_g_workspace(int64_t obs, int64_t vars, int& nchunks, int64_t& chunk);
+// G = X^T X workspace; nchunks = rows of the fused first-sweep g0 partials
+int64_t gram_g_workspace(int dtype, int64_t obs, int64_t vars, int& nchunks, int64_t& chunk);
+// tcgen05 (kind::tf32) G for fp32 inputs, vars <= 256 (bak_gram_tc.cu)
+bool gram_tc_enabled(int dtype, int64_t vars);
+int64_t gram_tc_workspace(int64_t obs, int64_t vars);
+int launch_gram_g_tc(const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
+                     int64_t part_bytes, cudaStream_t st, void* norms_out, const void* e, double* g0,
+                     int64_t* status);
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
                   int64_t part_bytes, cudaStream_t st, void* norms_out = nullptr, const void* e = nullptr,
                   double* g0 = nullptr);

@@ -40,7 +40,7 @@ def _pin_inputs(g, x, y):
     assert _sha(y) == str(g["sha_y"])
 
 
-def _check(rep, g, x, y, tol):
+def _check(rep, g, x, y, tol, hist_tol=None):
     assert rep.sweeps_run == int(g["sweeps_run"])
     assert rep.converged == bool(g["converged"])
     assert rep.drift_warning == bool(g["drift_warning"])
@@ -53,8 +53,12 @@ def _check(rep, g, x, y, tol):
     href = np.asarray(g["history"], np.float64)
     assert h.shape == href.shape
     # history holds sum e^2 per sweep (bak.py:106-108); absolute floor (tol ||y||)^2 for the
-    # sweeps at the rounding floor (C4's maintained e reaches exactly 0 in the reference)
-    assert np.all(np.abs(h - href) <= tol * href + (tol * float(g["ynorm_f64"])) ** 2)
+    # sweeps at the rounding floor (C4's maintained e reaches exactly 0 in the reference).
+    # fp32: the reference's history is an fp32 np.dot over 2^24 terms, whose own rounding
+    # is ~1e-3 (its last entry 1677.819 vs 1677.932 = the fp64 ||y - x a||^2 of its own a);
+    # the GPU sums e^2 in fp64, so the bar there is hist_tol = 5e-3
+    ht = tol if hist_tol is None else hist_tol
+    assert np.all(np.abs(h - href) <= ht * href + (tol * float(g["ynorm_f64"])) ** 2)
     rn = orc.residual_norm_f64(x, y, rep.a_hat)
     rref = float(g["resid_norm_f64"])
     ynorm = float(g["ynorm_f64"])
@@ -104,7 +108,9 @@ def test_c3_fp32_full_matches_reference(c3_single, variant):
     g, x, y, dm = c3_single
     rep = pb.solve_bak(dm, y, pb.SolveConfig(max_iter=20, tol=0, record_history=True), variant=variant)
     assert rep.variant == ("gram" if variant in ("auto", "gram") else "stream")
-    _check(rep, g, x, y, 1e-4)
+    _check(rep, g, x, y, 1e-4, hist_tol=5e-3)
+    # the GPU's fp64 history is the squared fp64 residual norm of its own a
+    assert abs(rep.residual_norm_history[-1] - float(g["resid_norm_f64"]) ** 2) <= 1e-4 * rep.residual_norm_history[-1]
 
 
 def test_c4_full_ten_sweeps_matches_reference():

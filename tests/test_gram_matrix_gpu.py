@@ -49,9 +49,65 @@ def test_gram_matrix_fp32_3xtf32_and_dmma(obs, nv, monkeypatch):
     # diagonal (the column norms the solve divides by) to a few 2^-21
     d_err = np.max(np.abs(np.diag(G3) - np.diag(ref)) / np.diag(ref))
     assert d_err <= 4e-6, d_err
+    # the legacy mma.sync 3xTF32 kernel (BAK_GRAM_G=x3) meets the same bar
+    Gx = _gram(x, monkeypatch, {"BAK_GRAM_G": "x3"})
+    errx = np.linalg.norm(Gx - ref) / np.linalg.norm(ref)
+    assert errx <= 2e-6, errx
     Gd = _gram(x, monkeypatch, {"BAK_GRAM_G": "dmma"})
     errd = np.linalg.norm(Gd - ref) / np.linalg.norm(ref)
     assert errd <= 1e-13, errd
+
+
+@pytest.mark.parametrize("obs,nv,chunk", [(1000, 7, None), (50_001, 64, None), (131_071, 130, None),
+                                          (200_000, 256, None), (100_003, 200, "32"), (300_000, 256, "65536")])
+def test_gram_fp32_tcgen05_with_fused_first_dots(obs, nv, chunk, monkeypatch):
+    """fp32 G on tcgen05 (kind::tf32, TMEM): G and the fused g0 = X^T e against
+    fp64 numpy; ragged rows / columns, vb = 128 and 256, one-tile and large chunks."""
+    import torch
+    import paper_2104_12570_b200 as pb
+    from paper_2104_12570_b200 import _lib
+    from paper_2104_12570_b200.bak import _Workspace, _stream_ptr
+    if chunk:
+        monkeypatch.setenv("BAK_GRAM_TC_CHUNK", chunk)
+    rng = np.random.default_rng(obs + nv)
+    x = np.asfortranarray(rng.standard_normal((obs, nv)).astype(np.float32))
+    e = rng.standard_normal(obs).astype(np.float32)
+    xd = x.astype(np.float64)
+    ref = xd.T @ xd
+    gref = xd.T @ e.astype(np.float64)
+    lib = _lib.load()
+    dm = pb.to_device_matrix(x)
+    dev = dm.data.device
+    ed = torch.from_numpy(e).to(dev)
+    G = torch.empty((nv, nv), dtype=torch.float64, device=dev)
+    rows = int(lib.bak_gram_dot_rows(dm.code, obs, nv))
+    assert rows == 1  # the tcgen05 path reduces the fused dots to one row
+    g0 = torch.zeros((rows, nv), dtype=torch.float64, device=dev)
+    ws = _Workspace(torch, dev, lib.bak_gram_matrix_workspace(dm.code, obs, nv))
+    st = _stream_ptr(torch, dev)
+    _lib.check(lib.bak_gram_matrix_dot(dm.code, dm.ptr, obs, nv, dm.ldx, G.data_ptr(), ed.data_ptr(), g0.data_ptr(),
+                                       ws.ptr, ws.nbytes, st), "bak_gram_matrix_dot")
+    Gh, gh = G.cpu().numpy(), g0.cpu().numpy()[0]
+    assert np.array_equal(Gh, Gh.T)
+    # off-diagonal: the tensor core's truncating fp32 accumulation over C rows leaves an
+    # entry low by ~1.2e-8 * C of itself (default C = 1024; tools/gram_tc_probe.py)
+    c = int(chunk or 1024)
+    off = ~np.eye(nv, dtype=bool)
+    off_err = np.max(np.abs(Gh - ref)[off] / np.sqrt(np.outer(np.diag(ref), np.diag(ref)))[off])
+    assert off_err <= max(2e-6, 4e-8 * c) / np.sqrt(obs) * 40, off_err
+    err = np.linalg.norm(Gh - ref) / np.linalg.norm(ref)
+    assert err <= (2e-6 if c <= 4096 else 2e-5), err
+    # diagonal (the column norms the solve divides by): fp32 FMA chains per 32-row tile
+    d_err = np.max(np.abs(np.diag(Gh) - np.diag(ref)) / np.diag(ref))
+    assert d_err <= 1e-6, d_err
+    # fused first-sweep dots: fp32 FMA chains per 32-row tile, tiles summed in fp64
+    scale = np.sqrt(np.diag(ref) * float(e.astype(np.float64) @ e))
+    assert np.max(np.abs(gh - gref) / scale) <= 1e-6
+    # deterministic
+    G2 = torch.empty_like(G)
+    _lib.check(lib.bak_gram_matrix(dm.code, dm.ptr, obs, nv, dm.ldx, G2.data_ptr(), ws.ptr, ws.nbytes, st),
+               "bak_gram_matrix")
+    assert torch.equal(G, G2)
 
 
 def test_batched_wave_is_whole_sms():

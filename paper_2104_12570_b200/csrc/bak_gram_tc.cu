@@ -19,7 +19,7 @@
 // fp64), so only the off-diagonal entries carry the ~1e-5-of-themselves
 // truncation (for near-orthogonal columns ~1e-8 of the diagonal).
 //
-// One CTA per SM, persistent over the row chunks; 6 warps:
+// One CTA per SM, persistent over the row chunks; 10 warps:
 //   warp 0     TMA producer: 32-row x vb-column tiles of column-major x (2-D
 //              tensor map, 128B swizzle = the UMMA K-major SW128 layout, rows
 //              past obs / columns past vars zero-filled) and the tile's 32
@@ -28,12 +28,14 @@
 //              per 8-row k-step 2 (vb=128) or 4 (vb=256) tcgen05.mma
 //              M=128 x N=vb x K=8 into two 128 x 256 fp32 accumulators;
 //              tcgen05.commit frees the ring slot / signals the epilogue;
-//   warps 2-5  split each tile in place (hi over the raw tile, 2*lo into a
-//              second buffer with the same swizzled layout — the split is
-//              element-wise, so the swizzle does not matter), accumulate
-//              x_j . e and x_j . x_j in fp64 for 2 columns per thread, drain the
-//              accumulators (tcgen05.ld 32x32b, warp w reads TMEM lanes
-//              32*(w%4)..) into the chunk's partial S.
+//   warps 2-9  split each tile in place, one column per thread (hi over the
+//              raw tile, 2*lo into a second buffer with the same swizzled
+//              layout — the split is element-wise, so the swizzle does not
+//              matter), accumulate x_j . e and x_j . x_j, and drain the
+//              accumulators (tcgen05.ld 32x32b; warp w reads TMEM lanes
+//              32*(w%4).., two warps per quadrant split the columns) into the
+//              chunk's partial S.  Waits sleep in mbarrier.try_wait with a
+//              suspend-time hint instead of spinning on issue slots.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -50,9 +52,9 @@ namespace {
 
 constexpr int kTK = 32;          // rows per tile: 32 fp32 = one 128-byte swizzle row
 constexpr int kStages = 3;       // ring depth
-constexpr int kConvWarps = 4;    // split / epilogue warps (one per TMEM lane quadrant)
+constexpr int kConvWarps = 8;    // split / epilogue warps (two per TMEM lane quadrant)
 constexpr int kThreads = 64 + 32 * kConvWarps;
-constexpr int kReduceGroups = 16;
+constexpr int kReduceGroups = 32;
 
 struct TcParams {
   int64_t obs;
@@ -116,14 +118,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// try_wait with a suspend-time hint: the thread sleeps in the barrier unit
+// until the phase completes (or ~20 us pass) instead of spinning on issue slots
+__device__ __forceinline__ bool mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(20000u)
+      : "memory");
+  return ok != 0;
+}
+
 // wait on an mbarrier phase; after the deadline (or once another role gave up)
 // report BAK_ETIMEOUT and let every role fall through to the teardown
 __device__ __forceinline__ bool wait_phase(uint64_t* bar, uint32_t parity, volatile int* abort_flag,
                                            int64_t* status) {
-  if (*abort_flag) return false;
   if (mbar_test(bar, parity)) return true;
   const uint64_t t0 = globaltimer();
-  while (!mbar_test(bar, parity)) {
+  while (!mbar_wait_hint(bar, parity)) {
     if (*abort_flag) return false;
     if (globaltimer() - t0 > kTimeoutNs) {
       report_error(status, BAK_ETIMEOUT);
@@ -158,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 32 * kConvWarps);
+      mbar_init(&conv[s], vb == 256 ? 256 : 128);  // the converting threads
       mbar_init(&empty[s], 1);
     }
     mbar_init(accf, 1);
@@ -239,27 +254,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // -------------------- split / g0 / epilogue (warps 2..5) --------------------
-    const int ct = tid - 64;  // 0..127
-    const int quad = warp & 3;
-    const int ncol = vb / 128;  // columns per thread: ct (+128)
+    // -------------------- split / g0 / epilogue (warps 2..9) --------------------
+    const int ct = tid - 64;  // 0..255: the split of column ct (vb = 128: threads 0..127)
+    const int quad = warp & 3;      // TMEM lane quadrant this warp may read
+    const int whalf = (warp - 2) >> 2;  // which half of the column blocks it drains
+    const bool splitter = ct < vb;
+    const int ncol = vb / 128;  // accumulators (M halves)
     int s = 0;
     uint32_t ph = 0;
     int64_t it = 0;
     for (int64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x, ++it) {
-      double g0a[2] = {0.0, 0.0}, d2a[2] = {0.0, 0.0};
+      double g0a[1] = {0.0}, d2a[1] = {0.0};
       const int nt = chunk_tiles(c);
       for (int t = 0; t < nt; ++t) {
-        if (!wait_phase(&full[s], ph, abort_flag, p.status)) goto done;
-        unsigned char* r_t = raw + s * tile_bytes;
-        unsigned char* l_t = lo + s * tile_bytes;
-        const float* e_t = es + s * kTK;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h >= ncol) break;
-          const int col = ct + 128 * h;
-          // per tile: x_j . x_j and x_j . e over the tile's 32 rows in fp32 (FMA
-          // chains of 32), then one widening add into the fp64 chunk totals
+        if (splitter) {
+          if (!wait_phase(&full[s], ph, abort_flag, p.status)) goto done;
+          unsigned char* r_t = raw + s * tile_bytes;
+          unsigned char* l_t = lo + s * tile_bytes;
+          const float* e_t = es + s * kTK;
+          const int col = ct;
+          // x_j . x_j and x_j . e over the tile's 32 rows in fp32 (FMA chains
+          // of 32), then one widening add into the fp64 chunk totals
           float d2t = 0.f, g0t = 0.f;
 #pragma unroll
           for (int q = 0; q < kTK / 4; ++q) {
@@ -288,21 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               g0t = __fmaf_rn(v.w, e4.w, g0t);
             }
           }
-          d2a[h] += static_cast<double>(d2t);
-          if (p.with_e) g0a[h] += static_cast<double>(g0t);
+          d2a[0] += static_cast<double>(d2t);
+          if (p.with_e) g0a[0] += static_cast<double>(g0t);
+          fence_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+          mbar_arrive(&conv[s]);
         }
-        fence_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
-        mbar_arrive(&conv[s]);
         if (++s == kStages) { s = 0; ph ^= 1u; }
       }
-      {
+      if (splitter) {
         double* g = p.cpart + c * 2 * vb;
         if (p.with_e) g[ct] = g0a[0];
         g[vb + ct] = d2a[0];
-        if (ncol == 2) {
-          if (p.with_e) g[ct + 128] = g0a[1];
-          g[vb + ct + 128] = d2a[1];
-        }
       }
       // epilogue: this chunk's S -> HBM (fp32), rows 32*quad + lane of each accumulator
       if (!wait_phase(accf, static_cast<uint32_t>(it & 1), abort_flag, p.status)) goto done;
@@ -311,7 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int a = 0; a < ncol; ++a) {
         const int row = a * 128 + quad * 32 + lane;
         float4* dst = reinterpret_cast<float4*>(out + static_cast<int64_t>(row) * vb);
-        for (int cb = 0; cb < vb / 16; ++cb) {
+        const int nblk = vb / 16;
+        for (int cb = whalf * (nblk / 2); cb < (whalf + 1) * (nblk / 2); ++cb) {
           float v[16];
           tmem_ld16(tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * 256 + cb * 16), v);
 #pragma unroll
@@ -331,45 +343,52 @@ done:
   }
 }
 
-// red[g][e] = sum over chunks [g*per, (g+1)*per) of part[c][e], chunk order, fp64
-__global__ void gram_tc_reduce1(const float* __restrict__ part, int64_t nchunks, int64_t E, double* __restrict__ red) {
+// red[g][e] = sum over chunks [g*per, (g+1)*per) of part[c][e], chunk order, fp64;
+// the last 2*vb "elements" of each group row are the fp64 per-chunk
+// x_j . e / x_j . x_j partials (cpart), reduced the same way
+__global__ void gram_tc_reduce1(const float* __restrict__ part, const double* __restrict__ cpart, int64_t nchunks,
+                                int64_t E, int vb, double* __restrict__ red) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int g = blockIdx.y;
   const int64_t per = (nchunks + gridDim.y - 1) / gridDim.y;
   const int64_t c0 = g * per, c1 = imin64(nchunks, c0 + per);
-  if (e >= E) return;
+  const int64_t W = E + 2 * vb;
+  if (e >= W) return;
   double s = 0.0;
-  for (int64_t c = c0; c < c1; ++c) s += static_cast<double>(part[c * E + e]);
-  red[g * E + e] = s;
+  if (e < E) {
+    for (int64_t c = c0; c < c1; ++c) s += static_cast<double>(part[c * E + e]);
+  } else {
+    for (int64_t c = c0; c < c1; ++c) s += cpart[c * 2 * vb + (e - E)];
+  }
+  red[g * W + e] = s;
 }
 
 // G (vars x vars, column-major, symmetric) = (T + T^T)/2 off the diagonal,
-// with T = sum of the groups in order; diag G = norms = the chunk-ordered fp64
-// sums of x_j . x_j; g0 (one row) = chunk-ordered sum of the x_j . e partials
+// with T = sum of the groups in order; diag G = norms = the fp64 sums of
+// x_j . x_j; g0 (one row) = the fp64 sums of x_j . e (groups in order)
 __global__ void gram_tc_reduce2(const double* __restrict__ red, int ngroups, int vb, int64_t vars,
-                                double* __restrict__ G, float* __restrict__ norms, const double* __restrict__ cpart,
-                                int64_t nchunks, double* __restrict__ g0) {
-  const int64_t E = static_cast<int64_t>(vb) * vb;
+                                double* __restrict__ G, float* __restrict__ norms, double* __restrict__ g0) {
+  const int64_t E = static_cast<int64_t>(vb) * vb, W = E + 2 * vb;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx < vars * vars) {
     const int64_t i = idx % vars, j = idx / vars;  // G(i, j), column-major
     if (i == j) {
       double d = 0.0;
-      for (int64_t c = 0; c < nchunks; ++c) d += cpart[(2 * c + 1) * vb + i];
+      for (int g = 0; g < ngroups; ++g) d += red[g * W + E + vb + i];
       G[j * vars + i] = d;
       if (norms) norms[i] = static_cast<float>(d);
     } else {
       double tij = 0.0, tji = 0.0;
       for (int g = 0; g < ngroups; ++g) {
-        tij += red[g * E + i * vb + j];
-        tji += red[g * E + j * vb + i];
+        tij += red[g * W + i * vb + j];
+        tji += red[g * W + j * vb + i];
       }
       G[j * vars + i] = 0.5 * (tij + tji);
     }
   }
   if (g0 && idx < vars) {
     double s = 0.0;
-    for (int64_t c = 0; c < nchunks; ++c) s += cpart[2 * c * vb + idx];
+    for (int g = 0; g < ngroups; ++g) s += red[g * W + E + idx];
     g0[idx] = s;
   }
 }
@@ -390,7 +409,7 @@ TcSplit tc_split(int64_t obs, int64_t vars) {
   const int64_t E = static_cast<int64_t>(t.vb) * t.vb;
   t.part_bytes = round_up(t.nchunks * E * 4, 256);
   t.c_bytes = round_up(t.nchunks * 2 * t.vb * 8, 256);
-  t.red_bytes = round_up(kReduceGroups * E * 8, 256);
+  t.red_bytes = round_up(kReduceGroups * (E + 2 * t.vb) * 8, 256);
   return t;
 }
 
@@ -468,11 +487,12 @@ int launch_gram_g_tc(const void* x, int64_t obs, int64_t ldx, int64_t vars, doub
   BAK_CHECK_CUDA(cudaGetLastError());
   const int64_t E = static_cast<int64_t>(t.vb) * t.vb;
   const int groups = static_cast<int>(imin64(kReduceGroups, t.nchunks));
-  gram_tc_reduce1<<<dim3(static_cast<unsigned>((E + 255) / 256), groups), 256, 0, st>>>(part, t.nchunks, E, red);
+  gram_tc_reduce1<<<dim3(static_cast<unsigned>((E + 2 * t.vb + 255) / 256), groups), 256, 0, st>>>(
+      part, cpart, t.nchunks, E, t.vb, red);
   BAK_CHECK_CUDA(cudaGetLastError());
   const int64_t n2 = vars * vars;
   gram_tc_reduce2<<<static_cast<unsigned>((n2 + 255) / 256), 256, 0, st>>>(
-      red, groups, t.vb, vars, G, static_cast<float*>(norms_out), cpart, t.nchunks, with_e ? g0 : nullptr);
+      red, groups, t.vb, vars, G, static_cast<float*>(norms_out), with_e ? g0 : nullptr);
   BAK_CHECK_CUDA(cudaGetLastError());
   count_launches(3);
   return BAK_OK;

@@ -62,6 +62,10 @@ CONFIGS = {
                desc="very tall fp64 2^24x256, 20 sweeps", variant="gram", exact="stream"),
     "c3f32": dict(kind="system", obs=1 << 24, vars=256, dtype="f32", sweeps=20, tol=0.0, noise=0.01,
                   desc="very tall fp32 2^24x256, 20 sweeps", variant="gram", exact="stream"),
+    # one GPU's row shard of C3 at N=8 (2^24 / 8 rows): the EXACT per-column sweep with e on chip
+    "c3s8": dict(kind="system", obs=1 << 21, vars=256, dtype="f64", sweeps=20, tol=0.0, noise=0.01,
+                 desc="C3's per-GPU row shard at N=8: 2^21x256 fp64, 20 sweeps, exact on-chip sweep (e in "
+                      "registers across 120 CTAs, x through a quarter-column TMA ring)"),
     "c4": dict(kind="c4", obs=1000, vars=1_000_000, dtype="f64", sweeps=10, tol=0.0,
                desc="wide fp64 1,000x1,000,000, 10 sweeps"),
     "c5": dict(kind="batched", obs=512, vars=32, nsys=65536, dtype="f32", sweeps=200, tol=0.0, noise=0.01,

@@ -174,6 +174,10 @@ extern "C" int bak_sweep(int dtype, int variant, const void* x, int64_t obs, int
     prm.rows_per_cta = pl.rows_per_cta;
     prm.stage_elems = pl.stage_elems;
     prm.nstages = pl.nstages;
+    if (getenv("BAK_DEBUG"))
+      fprintf(stderr, "bak: plan variant=%d parts=%d threads=%d e=%d stages=%d rows/cta=%lld cluster=%d xs=%d\n",
+              pl.variant, pl.nparticipants, pl.nthreads, pl.e, pl.nstages, (long long)pl.rows_per_cta, pl.cluster,
+              pl.xs);
     return launch_onchip(dtype, pl, prm, st);
   }
   set_error("bak_sweep: variant %d not available", variant);

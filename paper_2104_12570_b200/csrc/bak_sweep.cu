@@ -106,7 +106,14 @@ __device__ __forceinline__ T quotient(T a, T b, T r) {
   } while (0)
 #endif
 
-template <typename T, int E, int MODE, int MAXNT>
+// XS (x from shared memory, for row blocks too large to keep two columns of x
+// in registers next to e — up to ~2.2M fp64 rows on one GPU): e stays in
+// registers (E rows per thread), the ring holds QUARTER columns (slot = the
+// rows of E/4 of each thread's row slots), the fused update/dot reads x_t and
+// x_{t+1} straight from the ring, and each consumer warp hands a quarter of
+// x_t back to the producer as soon as it has read it — so the load of x_{t+2}
+// starts during step t's arithmetic and overlaps the exchange that follows.
+template <typename T, int E, int MODE, int MAXNT, bool XS = false>
 __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams prm) {
 #ifdef BAK_PHASES
   long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], XS ? static_cast<uint32_t>(nwarps) : 1u);  // XS: one arrive per consumer warp
     }
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
@@ -182,7 +189,72 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   const int64_t ncols = prm.ncols;
   const int64_t total = prm.max_iter * ncols;
 
-  if (tid >= NT) {
+  if (tid >= NT && XS) {
+    // ======================= producer warp (XS: quarter columns) =======================
+    constexpr int NQ = 4;
+    const int64_t QR = static_cast<int64_t>(E / NQ) * NT;  // rows per quarter slot
+    const uint64_t pol = policy_evict_first();
+    int64_t f = 0;  // fills issued (4 per column step)
+    int sl = 0;     // its ring slot and the parity of that slot's next fill
+    uint32_t fph = 0;
+    bool halted = false;
+    for (int64_t u0 = 0; u0 < total && !halted; u0 += 32) {
+      const int64_t ul = u0 + lane;
+      int64_t cl = 0;
+      T n2l = T(1);
+      if (ul < total) {
+        const int64_t sw = ul / ncols, k = ul - sw * ncols;
+        cl = prm.cols ? static_cast<int64_t>(prm.cols[sw * prm.cols_stride + k]) : k;
+        n2l = n2g[cl];
+      }
+      const T ril = Num<T>::div(T(1), n2l);
+      const int nb = static_cast<int>(imin64(32, total - u0));
+      for (int i = 0; i < nb; ++i) {
+        const int64_t c = __shfl_sync(0xffffffffu, cl, i);
+        const T n2 = __shfl_sync(0xffffffffu, n2l, i);
+        const T ri = __shfl_sync(0xffffffffu, ril, i);
+        if (lane == 0) {
+          for (int q = 0; q < NQ && !halted; ++q) {
+            if (f >= S) {
+              const uint32_t par = fph ^ 1u;
+              if (!mbar_test(&empty[sl], par)) {
+                const uint64_t t0 = globaltimer();
+                while (!mbar_test(&empty[sl], par)) {
+                  if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+                }
+              }
+              if (halted) break;
+            }
+            if (q == 0) {
+              StageMeta& m = meta[(u0 + i) % kMaxStages];
+              m.col = c;
+              m.n2 = static_cast<double>(n2);
+              m.rinv = static_cast<double>(ri);
+            }
+            const int64_t rq = imax64(0, imin64(nrows - q * QR, QR));
+            const uint32_t bq = static_cast<uint32_t>(((rq + VEC - 1) / VEC) * VEC * sizeof(T));
+            mbar_arrive_expect_tx(&full[sl], bq);  // release: the column record is visible with the phase
+            if (bq) bulk_g2s(xs + static_cast<size_t>(sl) * prm.stage_elems, x + c * prm.ldx + r0 + q * QR, bq,
+                             &full[sl], pol);
+            ++f;
+            if (++sl == S) {
+              sl = 0;
+              fph ^= 1u;
+            }
+          }
+        }
+        halted = __shfl_sync(0xffffffffu, halted, 0);
+        if (halted) break;
+      }
+    }
+    if (lane == 0) {  // the last min(S, f) copies must land before this CTA exits
+      for (int64_t v = imax64(0, f - S); v < f; ++v) {
+        const uint64_t t0 = globaltimer();
+        while (!mbar_test(&full[v % S], static_cast<uint32_t>((v / S) & 1)))
+          if (globaltimer() - t0 > kTimeoutNs) break;
+      }
+    }
+  } else if (tid >= NT) {
     // =========================== producer warp ===========================
     // The whole warp prepares the next 32 schedule steps at once (lane l:
     // column index, n2 and 1/n2 of step u0 + l — the dependent global load and
@@ -247,7 +319,7 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   } else {
     // =========================== consumers ===============================
     const int kv = static_cast<int>(imax64(0, imin64(E, (nrows - tid + NT - 1) / NT)));
-    T ev[E], xc[E], xn[E];
+    T ev[E], xc[XS ? 1 : E], xn[XS ? 1 : E];
 #pragma unroll
     for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? eg[r0 + tid + static_cast<int64_t>(k) * NT] : T(0);
 
@@ -290,11 +362,12 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
 
     // fixed-order tree over the per-warp partials in shared memory
     auto warp_partials = [&](const T* v) -> T {
-      T a[kMaxWarps];
+      constexpr int kTree = kMaxWarps <= 1 ? 1 : (kMaxWarps <= 2 ? 2 : (kMaxWarps <= 4 ? 4 : 8));  // pow2 >= warps
+      T a[kTree];
 #pragma unroll
-      for (int w = 0; w < kMaxWarps; ++w) a[w] = (w < nwarps) ? v[w] : T(0);
+      for (int w = 0; w < kTree; ++w) a[w] = (w < nwarps) ? v[w] : T(0);
 #pragma unroll
-      for (int h = kMaxWarps / 2; h >= 1; h >>= 1)
+      for (int h = kTree / 2; h >= 1; h >>= 1)
 #pragma unroll
         for (int w = 0; w < h; ++w) a[w] = Num<T>::add(a[w], a[w + h]);
       return a[0];
@@ -525,6 +598,153 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
       return any2;
     };
 
+    int64_t sweep = 0;
+    bool converged = false;
+    if constexpr (XS) {
+      constexpr int NQ = 4, EQ = E / NQ;
+      static_assert(E % NQ == 0, "XS: rows per thread must split into quarters");
+      const bool full_rows = kv == E;
+      const uint32_t xs0 = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
+      const uint32_t slot_bytes = static_cast<uint32_t>(prm.stage_elems * sizeof(T));
+      // ring position of a fill as (slot, parity) pairs advanced incrementally
+      // (no 64-bit division on the per-quarter critical path)
+      struct Pos {
+        int sl;
+        uint32_t par;
+      };
+      auto adv = [&](Pos p, int n) -> Pos {  // n <= S
+        p.sl += n;
+        if (p.sl >= S) {
+          p.sl -= S;
+          p.par ^= 1u;
+        }
+        return p;
+      };
+      auto slot_addr = [&](Pos p) -> uint32_t { return xs0 + static_cast<uint32_t>(p.sl) * slot_bytes; };
+      auto wait_fill = [&](Pos p) {
+        const int sl = p.sl;
+        const uint32_t par = p.par;
+        if (!mbar_test(&full[sl], par)) {
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test(&full[sl], par)) {
+            if (globaltimer() - t0 > kTimeoutNs) {
+              report_error(prm.status, BAK_ETIMEOUT);
+              my_abort = 1;
+              break;
+            }
+          }
+        }
+      };
+      auto release = [&](Pos p) {  // this warp is done reading that fill
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[p.sl]);
+      };
+      auto meta_of = [&](int64_t u, int64_t& c, T& n2, T& ri) {
+        const StageMeta& m = meta[u % kMaxStages];
+        c = m.col;
+        n2 = static_cast<T>(m.n2);
+        ri = static_cast<T>(m.rinv);
+      };
+      auto xval = [&](uint32_t a, int kk, int k) -> T {
+        return (full_rows || k < kv) ? lds<T>(a + static_cast<uint32_t>(kk * NT * sizeof(T))) : T(0);
+      };
+      // ---- prologue: the dot for column 0 ----
+      uint32_t rc = 0;
+      T P = T(0), Q = T(0);
+      int64_t c0 = 0, c1 = 0;
+      T n2_0 = T(1), ri_0 = T(1), n2_1 = T(1), ri_1 = T(1);
+      T acc[4] = {T(0), T(0), T(0), T(0)};
+      Pos pc{0, 0u};  // fill (t, 0)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const Pos pq = adv(pc, q);
+        wait_fill(pq);
+        const uint32_t a = slot_addr(pq);
+#pragma unroll
+        for (int kk = 0; kk < EQ; ++kk) {
+          const int k = q * EQ + kk;
+          acc[k & 3] = Num<T>::fma(xval(a, kk, k), ev[k], acc[k & 3]);
+        }
+      }
+      meta_of(0, c0, n2_0, ri_0);
+      T pv = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+      bool aborted = reduce(pv, T(0), false, rc++, -1, -1, P, Q);
+      const bool upd_warp = (rank == 0) && (warp == (nwarps > 1 ? 1 : 0));
+      T a0 = upd_warp ? ag[c0] : T(0);
+      int64_t k = 0, t = 0;
+      while (!aborted) {
+        PH(7);
+        const bool more = t + 1 < total;
+        const T d = quotient(P, n2_0, ri_0);
+        const bool last = (k == ncols - 1);
+        T ac[4] = {T(0), T(0), T(0), T(0)};
+        T a1 = T(0);
+        const Pos pn = adv(pc, NQ);  // fill (t + 1, 0)
+        if (more) {
+          wait_fill(pn);
+          meta_of(t + 1, c1, n2_1, ri_1);
+          if (upd_warp) a1 = ag[c1];  // its latency overlaps the update loop below
+        }
+        PH(0);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const Pos fc = adv(pc, q), fn = adv(pn, q);
+          if (more && q > 0) wait_fill(fn);
+          const uint32_t a_c = slot_addr(fc), a_n = slot_addr(fn);
+          // update with this quarter of x_t, hand the slot back, then the dot with
+          // the same quarter of x_{t+1} (per row the same two roundings and the
+          // same FMA order as the fused loop of the register-resident kernel)
+#pragma unroll
+          for (int kk = 0; kk < EQ; ++kk) {
+            const int kq = q * EQ + kk;
+            ev[kq] = Num<T>::sub(ev[kq], Num<T>::mul(xval(a_c, kk, kq), d));
+          }
+          release(fc);
+          if (more) {
+#pragma unroll
+            for (int kk = 0; kk < EQ; ++kk) {
+              const int kq = q * EQ + kk;
+              ac[kq & 3] = Num<T>::fma(xval(a_n, kk, kq), ev[kq], ac[kq & 3]);
+            }
+          }
+        }
+        PH(1);
+        pv = Num<T>::add(Num<T>::add(ac[0], ac[1]), Num<T>::add(ac[2], ac[3]));
+        T qv = T(0);
+        if (last) {
+          T qa[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+          for (int kk = 0; kk < E; ++kk) qa[kk & 3] = Num<T>::fma(ev[kk], ev[kk], qa[kk & 3]);
+          qv = Num<T>::add(Num<T>::add(qa[0], qa[1]), Num<T>::add(qa[2], qa[3]));
+        }
+        PH(2);
+        if (upd_warp) {
+          const T na = Num<T>::add(a0, d);
+          ag[c0] = na;
+          if (more) a0 = (c1 == c0) ? na : a1;  // a1 = ag[c1] was read before the store
+        }
+        PH(5);
+        if (reduce(pv, qv, last, rc++, -1, -1, P, Q)) break;
+        PH(6);
+        if (last) {
+          if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
+          ++sweep;
+          if (prm.thresh2 >= 0.0 && static_cast<double>(Q) <= prm.thresh2) {
+            converged = true;
+            break;
+          }
+          if (sweep == prm.max_iter) break;
+          k = 0;
+        } else {
+          ++k;
+        }
+        ++t;
+        pc = pn;
+        c0 = c1;
+        n2_0 = n2_1;
+        ri_0 = ri_1;
+      }
+    } else {
     // ---- prologue: columns 0 and 1 into registers, dot for column 0 ----
     uint32_t rc = 0;
     T P = T(0), Q = T(0);
@@ -547,8 +767,7 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     T a0 = upd_warp ? ag[c0] : T(0);
     T a1 = (upd_warp && total > 1) ? ag[c1] : T(0);
 
-    int64_t sweep = 0, k = 0, t = 0;
-    bool converged = false;
+    int64_t k = 0, t = 0;
     // one column step: update with xc (column t), dot with xn (column t+1), then
     // refill xc with column t+2 (its LDS latency overlaps the reduction).
     // Returns true when the solve ends.  Called with the two buffers swapped on
@@ -613,10 +832,18 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         if (step(xn, xc)) break;
       }
     }
+    }
 
+    {
+      // the row addresses are recomputed here from a laundered base: otherwise
+      // the compiler keeps the E 64-bit addresses of the initial load of e live
+      // across the whole solve (2E registers; E = 32 fp64 spilled)
+      T* ew = eg + r0 + tid;
+      asm volatile("mov.b64 %0, %0;" : "+l"(ew));
 #pragma unroll
-    for (int kk = 0; kk < E; ++kk)
-      if (kk < kv) eg[r0 + tid + static_cast<int64_t>(kk) * NT] = ev[kk];
+      for (int kk = 0; kk < E; ++kk)
+        if (kk < kv) ew[static_cast<int64_t>(kk) * NT] = ev[kk];
+    }
 #ifdef BAK_PHASES
     if (tid == 0 && rank == 0 && prm.history)
       for (int i = 0; i < 8; ++i) prm.history[prm.max_iter + i] = static_cast<double>(ph_acc[i]);
@@ -642,9 +869,9 @@ size_t smem_bytes(const SweepPlan& pl, size_t tsize) {
          kMaxStages * sizeof(StageMeta) + 2 * 2 * 32 * tsize + 16 + 2 * kMaxCluster * 16 + 16 + 32 + 16 + 16;
 }
 
-template <typename T, int E, int MODE, int MAXNT>
+template <typename T, int E, int MODE, int MAXNT, bool XS = false>
 int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
-  auto kern = sweep_kernel<T, E, MODE, MAXNT>;
+  auto kern = sweep_kernel<T, E, MODE, MAXNT, XS>;
   const size_t smem = smem_bytes(pl, sizeof(T));
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t cfg{};
@@ -707,8 +934,26 @@ int launch_e(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   return BAK_EUNSUPPORTED;
 }
 
+// XS plans: 7 consumer warps + the producer = 8 warps, two per SM sub-partition,
+// so a thread may hold up to 255 registers (9 warps cap it at 168: e spilled)
+constexpr int kXsConsumers = 224;
+
+template <typename T, int MODE>
+int launch_xs(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
+  if constexpr (MODE == kModeGrid || MODE == kModeGridCl) {
+    switch (pl.e) {
+      case 40: return launch_one<T, 40, MODE, kXsConsumers, true>(pl, prm, st);
+      case 56: return launch_one<T, 56, MODE, kXsConsumers, true>(pl, prm, st);
+      case 80: return launch_one<T, 80, MODE, kXsConsumers, true>(pl, prm, st);
+    }
+  }
+  set_error("bak_sweep: unsupported XS plan (rows per thread %d)", pl.e);
+  return BAK_EUNSUPPORTED;
+}
+
 template <typename T, int MODE>
 int launch_nt(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
+  if (pl.xs) return launch_xs<T, MODE>(pl, prm, st);
   if (pl.nthreads == 32) return launch_e<T, MODE, 32>(pl, prm, st);
   if (pl.nthreads <= 128) return launch_e<T, MODE, 128>(pl, prm, st);
   return launch_e<T, MODE, kMaxConsumers>(pl, prm, st);
@@ -778,6 +1023,39 @@ static bool plan_fill(int dtype, int variant, int64_t obs, int nthreads, int e, 
   return true;
 }
 
+// XS plan (GRID, x read from a quarter-column ring; e in registers): all
+// `parts` CTAs, rows spread evenly, E in {40, 56, 80} rows per thread of 224
+// consumers; at least 6 quarter slots (the 5 a step reads + 1 in flight).
+static bool plan_xs(int dtype, int64_t obs, int parts, int cluster, SweepPlan& pl) {
+  if (parts < 2) return false;
+  const size_t ts = dtype_size(dtype);
+  const size_t smem_cap = static_cast<size_t>(device_max_smem_optin()) - 2048;
+  const int64_t rpc = round_up((obs + parts - 1) / parts, 4);
+  if ((parts - 1) * rpc >= obs) return false;
+  for (int e : {40, 56, 80}) {
+    if (static_cast<int64_t>(kXsConsumers) * e < rpc) continue;
+    SweepPlan cand;
+    cand.variant = BAK_VARIANT_GRID;
+    cand.nthreads = kXsConsumers;
+    cand.e = e;
+    cand.nparticipants = parts;
+    cand.rows_per_cta = rpc;
+    cand.stage_elems = static_cast<int64_t>(e / 4) * kXsConsumers;
+    cand.cluster = cluster;
+    cand.xs = 1;
+    cand.nstages = 0;
+    const size_t fixed = smem_bytes(cand, ts);
+    const size_t slot = static_cast<size_t>(cand.stage_elems) * ts;
+    int st = static_cast<int>((smem_cap - fixed) / slot);
+    if (st > kMaxStages) st = kMaxStages;
+    if (st < 6) return false;
+    cand.nstages = st;
+    pl = cand;
+    return true;
+  }
+  return false;
+}
+
 // BAK_PLAN="parts,e,nthreads" overrides the heuristic (tuning experiments)
 static bool plan_env(int dtype, int variant, int64_t obs, SweepPlan& pl) {
   const char* env = getenv("BAK_PLAN");
@@ -821,8 +1099,16 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl, bool force_
     // evenly over a multiple of kGridCluster CTAs.  BAK_GRID_FLAT=1: one level.
     const char* flat = getenv("BAK_GRID_FLAT");
     const int max_parts = kGridCluster * (grid_cluster_capacity() < 32 ? grid_cluster_capacity() : 32);
+    const char* xs_env = getenv("BAK_GRID_XS");  // tuning aid: "1" = XS plans first
+    if (xs_env && xs_env[0] == '1' && !force_flat && !(flat && flat[0] == '1') && coop_clusters_ok() &&
+        plan_xs(dtype, obs, static_cast<int>(imin64(sms, max_parts)) / kGridCluster * kGridCluster, kGridCluster, pl))
+      return true;
+    // fp64 register plans past E = 16 spill (3E doubles per thread); the XS plan
+    // (e in registers, x from the shared ring) is faster there (tools/grid_compare.py)
+    const int max_reg_e = dtype == BAK_F64 ? 16 : 32;
     if (!force_flat && !(flat && flat[0] == '1') && coop_clusters_ok()) {
       for (int e : kEs) {
+        if (e > max_reg_e) break;
         const int64_t rows = 256LL * e;
         const int64_t parts = round_up((obs + rows - 1) / rows, kGridCluster);
         if (parts > sms || parts > max_parts) continue;
@@ -838,14 +1124,19 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl, bool force_
         return true;
       }
     }
+    const bool two_level = !force_flat && !(flat && flat[0] == '1') && coop_clusters_ok();
+    if (two_level && plan_xs(dtype, obs, static_cast<int>(imin64(sms, max_parts)) / kGridCluster * kGridCluster,
+                             kGridCluster, pl))
+      return true;
     for (int nt : {256}) {
       for (int e : kEs) {
+        if (e > max_reg_e && two_level) break;  // the two-level XS plan did not fit either
         const int64_t rows = static_cast<int64_t>(nt) * e;
         const int64_t parts = (obs + rows - 1) / rows;
         if (parts <= sms && plan_fill(dtype, variant, obs, nt, e, static_cast<int>(parts), pl, 3)) return true;
       }
     }
-    return false;
+    return plan_xs(dtype, obs, static_cast<int>(imin64(sms, kGridSlotsMax)), 0, pl);
   }
   return false;
 }

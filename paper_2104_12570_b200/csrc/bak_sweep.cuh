@@ -39,6 +39,7 @@ struct SweepPlan {
   int64_t rows_per_cta = 0;
   int64_t stage_elems = 0;
   int cluster = 0;  // GRID: CTAs per cluster of the two-level exchange (0 = one level)
+  int xs = 0;       // GRID: x read from a quarter-column shared-memory ring (rows past register capacity)
 };
 
 // force_flat: GRID plans use the one-level exchange (as BAK_GRID_FLAT=1)

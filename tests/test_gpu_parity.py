@@ -115,8 +115,12 @@ def test_deterministic_bits():
 
 
 def test_tall_stream_matches_oracle():
+    """Past the on-chip capacity (XS plans hold 2.15M fp64 rows with the two-level
+    exchange, 2.65M with the one-level one) with fewer than
+    4 sweeps, "auto" runs the exact STREAM kernel (GRAM needs >= 4 sweeps to pay
+    for G = X^T X)."""
     pb = _pb()
-    x, y, _ = orc.config_c3(obs=1 << 21, nvars=32, precision="double")
+    x, y, _ = orc.config_c3(obs=2_700_000, nvars=32, precision="double")
     ref = orc.solve(x, y, max_iter=3, tol=0)
     rep = pb.solve_bak(x, y, pb.SolveConfig(max_iter=3, tol=0))
     assert rep.variant == "stream"
@@ -402,3 +406,26 @@ def test_batched_pipelined_host_upload_bit_identical():
     s = 1234
     ref = orc.solve(hx[s].numpy().T, hy[s].numpy(), max_iter=20, tol=0)
     assert orc.rel_coeff_err(r_pipe.a_hat[s], ref["a_hat"]) <= 1e-4
+
+
+@pytest.mark.parametrize("obs,nv,precision", [(1_100_003, 6, "double"), (2_097_152, 5, "double"),
+                                              (1_600_001, 4, "double"), (2_000_000, 5, "single")])
+def test_xs_exact_sweep_tall_matches_oracle(obs, nv, precision):
+    """The exact on-chip sweep for row blocks past register capacity (GRID, x read
+    from the quarter-column ring, e in registers): 1.1M-2.1M rows on one GPU,
+    ragged rows, against the oracle; random ordering and an early break too."""
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=obs, nvars=nv, precision=precision)
+    tol = TOL[np.dtype(x.dtype)]
+    cfg = dict(max_iter=3, tol=0, record_history=True)
+    ref = orc.solve(x, y, **cfg)
+    rep = pb.solve_bak(x, y, pb.SolveConfig(**cfg), variant="grid")
+    assert rep.variant == "grid" and rep.sweeps_run == 3
+    assert orc.rel_coeff_err(rep.a_hat, ref["a_hat"]) <= tol
+    np.testing.assert_allclose(rep.residual_norm_history, ref["residual_norm_history"], rtol=max(1e3 * tol, 1e-6))
+    if precision == "double" and nv == 6:
+        cfg2 = dict(max_iter=20, tol=1e-3, ordering="random", ordering_seed=5, record_history=True)
+        ref2 = orc.solve(x, y, **cfg2)
+        rep2 = pb.solve_bak(x, y, pb.SolveConfig(**cfg2), variant="grid")
+        assert rep2.sweeps_run == ref2["sweeps_run"] and rep2.converged == ref2["converged"]
+        assert orc.rel_coeff_err(rep2.a_hat, ref2["a_hat"]) <= tol

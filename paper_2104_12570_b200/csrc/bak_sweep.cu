@@ -50,7 +50,14 @@ namespace {
 constexpr int kModeCta = 0, kModeCluster = 1, kModeGrid = 2, kModeGridCl = 3;
 constexpr int kGridCluster = 8;  // CTAs per cluster in kModeGridCl (portable size)
 constexpr int kMaxCluster = 16;
-constexpr int kMaxStages = 16;
+constexpr int kMaxStages = 32;      // ring slots (XS plans use up to 32 sub-column slots)
+constexpr int kMaxRegStages = 16;   // register-resident plans: whole-column stages
+
+// XS: sub-stages per column.  Quarters: eighths were measured no faster at
+// 2^21 rows and slower at 2^20 (more waits / releases per column step,
+// profiles/r02_xs_phases.txt)
+template <int E>
+__host__ __device__ constexpr int xs_nq() { return 4; }
 constexpr int kMaxConsumers = 256;
 constexpr int kBarConsumers = 1;  // named barrier id used by consumer warps only
 
@@ -191,8 +198,8 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
 
   if (tid >= NT && XS) {
     // ======================= producer warp (XS: quarter columns) =======================
-    constexpr int NQ = 4;
-    const int64_t QR = static_cast<int64_t>(E / NQ) * NT;  // rows per quarter slot
+    constexpr int NQ = xs_nq<E>();
+    const int64_t QR = static_cast<int64_t>(E / NQ) * NT;  // rows per sub-column slot
     const uint64_t pol = policy_evict_first();
     int64_t f = 0;  // fills issued (4 per column step)
     int sl = 0;     // its ring slot and the parity of that slot's next fill
@@ -601,8 +608,8 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     int64_t sweep = 0;
     bool converged = false;
     if constexpr (XS) {
-      constexpr int NQ = 4, EQ = E / NQ;
-      static_assert(E % NQ == 0, "XS: rows per thread must split into quarters");
+      constexpr int NQ = xs_nq<E>(), EQ = E / NQ;
+      static_assert(E % NQ == 0, "XS: rows per thread must split into sub-column slots");
       const bool full_rows = kv == E;
       const uint32_t xs0 = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
       const uint32_t slot_bytes = static_cast<uint32_t>(prm.stage_elems * sizeof(T));
@@ -1016,16 +1023,17 @@ static bool plan_fill(int dtype, int variant, int64_t obs, int nthreads, int e, 
   const size_t stage_bytes = rows * ts;
   if (fixed + 2 * stage_bytes > smem_cap) return false;
   int s = static_cast<int>((smem_cap - fixed) / stage_bytes);
-  if (s > kMaxStages) s = kMaxStages;
+  if (s > kMaxRegStages) s = kMaxRegStages;
   if (s < min_stages) return false;
   cand.nstages = s;
   pl = cand;
   return true;
 }
 
-// XS plan (GRID, x read from a quarter-column ring; e in registers): all
-// `parts` CTAs, rows spread evenly, E in {40, 56, 80} rows per thread of 224
-// consumers; at least 6 quarter slots (the 5 a step reads + 1 in flight).
+// XS plan (GRID, x read from a sub-column ring; e in registers): all `parts`
+// CTAs, rows spread evenly, E in {40, 56, 80} rows per thread of 224
+// consumers, quarter-column slots (xs_nq); at least nq + 2 slots (the nq + 1
+// a step reads + 1 in flight).
 static bool plan_xs(int dtype, int64_t obs, int parts, int cluster, SweepPlan& pl) {
   if (parts < 2) return false;
   const size_t ts = dtype_size(dtype);
@@ -1040,7 +1048,8 @@ static bool plan_xs(int dtype, int64_t obs, int parts, int cluster, SweepPlan& p
     cand.e = e;
     cand.nparticipants = parts;
     cand.rows_per_cta = rpc;
-    cand.stage_elems = static_cast<int64_t>(e / 4) * kXsConsumers;
+    const int nq = 4;  // xs_nq<E>()
+    cand.stage_elems = static_cast<int64_t>(e / nq) * kXsConsumers;
     cand.cluster = cluster;
     cand.xs = 1;
     cand.nstages = 0;
@@ -1048,7 +1057,7 @@ static bool plan_xs(int dtype, int64_t obs, int parts, int cluster, SweepPlan& p
     const size_t slot = static_cast<size_t>(cand.stage_elems) * ts;
     int st = static_cast<int>((smem_cap - fixed) / slot);
     if (st > kMaxStages) st = kMaxStages;
-    if (st < 6) return false;
+    if (st < nq + 2) return false;  // the nq + 1 slots a step reads + 1 in flight
     cand.nstages = st;
     pl = cand;
     return true;

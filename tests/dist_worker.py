@@ -26,6 +26,14 @@ for variant in ("gram", "stream"):
     rep = solve_bak_rowsharded([np.asfortranarray(x[r0:r1])], [y[r0:r1]], cfg, comm, variant=variant)[0]
     ref = orc.solve(x, y, max_iter=5, tol=0)
     out[variant] = dict(err=orc.rel_coeff_err(rep.a_hat, ref["a_hat"]), sweeps=rep.sweeps_run, label=rep.variant)
+# C5-style system sharding: no communication on the data path, one gather at the end
+from paper_2104_12570_b200.sharded import solve_bak_batched_sharded  # noqa: E402
+nsys = 24
+xs = np.stack([orc.config_c5_system(k, obs=128, nvars=16)[0] for k in range(nsys)])
+ys = np.stack([orc.config_c5_system(k, obs=128, nvars=16)[1] for k in range(nsys)])
+s0, s1, brep = solve_bak_batched_sharded(xs, ys, pb.SolveConfig(max_iter=40, tol=0), comm, gather=True)
+errs = [orc.rel_coeff_err(brep.a_hat[k], orc.solve(xs[k], ys[k], max_iter=40, tol=0)["a_hat"]) for k in range(nsys)]
+out["batched"] = dict(nsys=int(brep.a_hat.shape[0]), err=max(errs), sweeps=int(brep.sweeps_run.min()))
 torch.distributed.barrier()
 torch.distributed.destroy_process_group()
 if rank == 0:

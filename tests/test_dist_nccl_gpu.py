@@ -13,16 +13,38 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+def _run(n):
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    from paper_2104_12570_b200 import launch
+    cmd = launch.torchrun_argv(n, os.path.join(here, "dist_worker.py"), [])
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+
+
 def test_nccl_rowsharded_solves_match_oracle():
     import torch
     n = max(1, min(torch.cuda.device_count(), 8))
-    here = os.path.dirname(os.path.abspath(__file__))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(here, "dist_worker.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    out = _run(n)
     assert out.returncode == 0, out.stderr[-3000:]
     line = [ln for ln in out.stdout.splitlines() if ln.startswith("RESULT ")][-1]
     res = json.loads(line[len("RESULT "):])
     assert res["gram"]["sweeps"] == 5 and res["gram"]["err"] <= 1e-10
     assert res["stream"]["sweeps"] == 5 and res["stream"]["err"] <= 1e-10
     assert res["stream"]["label"] == "stream-rowshard"
+    assert res["batched"]["nsys"] == 24 and res["batched"]["sweeps"] == 40 and res["batched"]["err"] <= 1e-4
+
+
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2", reason="needs 2 GPUs (this pool leases 1)")
+def test_two_gpus_exact_mailbox_exchange_and_system_shards():
+    """Two ranks on two GPUs: the exact row-sharded kernel's per-column
+    exchange crosses NVLink through the CUDA-IPC-mapped mailboxes; GRAM
+    all-gathers over NCCL; the batched systems shard with one final gather."""
+    out = _run(2)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("RESULT ")][-1]
+    res = json.loads(line[len("RESULT "):])
+    for v in ("gram", "stream"):
+        assert res[v]["sweeps"] == 5 and res[v]["err"] <= 1e-10
+    assert res["batched"]["err"] <= 1e-4

@@ -1,6 +1,6 @@
 # every BASELINE config through bench.py (one JSON line each) -> gpurun_out/bench_all.jsonl
 mkdir -p gpurun_out
 : > gpurun_out/bench_all.jsonl
-for c in c1 c2 c2b c4 c5 c3f32 c3 p1 p3; do
+for c in c1 c2 c2b c4 c5 c3f32 c3s8 c3 p1 p3; do
   timeout 900 python bench.py --config $c --steps 3 --warmup 3 ${BENCH_EXTRA} >> gpurun_out/bench_all.jsonl 2> gpurun_out/bench_$c.err || echo "{\"config\": \"$c\", \"failed\": true}" >> gpurun_out/bench_all.jsonl
 done

@@ -597,7 +597,8 @@ def run_ours(args, cfg, rank, world, dev):
         k_sweeps = int(status[0].item())
         xbytes = dm.obs * dm.vars * ts
         alg_bytes = xbytes * k_sweeps
-        kernel = f"sweep_kernel[{used}]"
+        kernel = ("bgram_kernel (block-Gram: 64-column blocks, one cluster reduction each, d = L^-1 g)"
+                  if used == "bgram" else f"sweep_kernel[{used}]")
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
     traffic = None
@@ -677,7 +678,8 @@ def run_ours(args, cfg, rank, world, dev):
         "config": {"workload": args.config, "desc": cfg["desc"], "obs": cfg["obs"], "vars": cfg["vars"],
                    "nsys": cfg.get("nsys", 1), "sweeps_per_step": cfg["sweeps"], "tol": cfg["tol"],
                    "thr": cfg.get("thr"),
-                   "variant": used + (" (labelled algebraically-equivalent sweep)" if used.startswith("gram") else ""),
+                   "variant": used + (" (labelled algebraically-equivalent sweep)" if used.startswith(("gram", "bgram"))
+                                      else ""),
                    "exact_variant": exact,
                    "rows_or_systems_per_rank": int(local_units),
                    "x_gb_per_sweep_total": round(cfg.get("nsys", 1) * cfg["obs"] * cfg["vars"] * ts / 1e9, 4),

@@ -37,6 +37,8 @@ extern "C" {
 #define BAK_VARIANT_GRID    3 /* persistent co-resident grid, e on chip, flag slots  */
 #define BAK_VARIANT_STREAM  4 /* persistent grid, e streamed through HBM             */
 #define BAK_VARIANT_GRAM    5 /* algebraically equal sweep via G = X^T X (labelled)  */
+#define BAK_VARIANT_BGRAM   6 /* block-Gram: 64-column blocks, one reduction each,
+                                  d_B = L_B^{-1} X_B^T e (labelled; cyclic order)   */
 
 /* status codes */
 #define BAK_OK           0

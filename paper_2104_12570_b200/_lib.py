@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("BAK_LIB_PATH") or os.path.join(_HERE, "libbak200.so")
 
 F32, F64 = 0, 1
 EDIVERGED = 6  # device status: the blocked sweep's divergence guard tripped
-VARIANTS = {"auto": 0, "cta": 1, "cluster": 2, "grid": 3, "stream": 4, "gram": 5}
+VARIANTS = {"auto": 0, "cta": 1, "cluster": 2, "grid": 3, "stream": 4, "gram": 5, "bgram": 6}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
 _i64 = ctypes.c_int64

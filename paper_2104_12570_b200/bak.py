@@ -301,6 +301,8 @@ def solve_bak(x, y, config: SolveConfig | None = None, a0=None, *, variant="auto
         raise ValueError(f"unknown variant {variant!r}, expected one of {tuple(_lib.VARIANTS)}")
     if variant == "auto":
         variant = _auto_variant(lib, x, cfg)
+    if variant == "bgram" and cfg.ordering != "cyclic":
+        raise ValueError("variant='bgram' (block-Gram, blocks of 64 consecutive columns) supports ordering='cyclic'")
     if variant == "gram" and _pipelinable(torch, x):
         return _solve_gram_pipelined(lib, torch, x, y, cfg, a0, device, return_device)
     dm = to_device_matrix(x, device)

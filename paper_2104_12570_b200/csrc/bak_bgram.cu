@@ -1,0 +1,595 @@
+// Block-Gram sweep (BAK_VARIANT_BGRAM; labelled, algebraically equal to the
+// per-column sweep — SURVEY §7.4-4) for systems whose residual fits on one
+// cluster and whose per-column cost is one dependent reduction (C1, C2, C4).
+//
+// One sweep of the reference (bak.py:92-112, cyclic order) visits columns in
+// blocks B = [j0, j0+64) and, within a block, runs
+//     d_j = <x_j, e_j> / n2_j,   e_{j+1} = e_j - d_j x_j
+// which in exact arithmetic equals
+//     g_B = X_B^T e_{j0}                     (dots against the block's first e)
+//     d_B = L_B^{-1} g_B,  L_B = lower triangle of G_BB = X_B^T X_B (diag n2)
+//     a_B += d_B ;  e -= X_B d_B              (per column, two roundings)
+// so a block needs ONE cluster reduction of 64 values instead of 64 dependent
+// ones.  M_B = L_B^{-1} (fp64, 64x64 per block, column-major) is computed once
+// per solve by bgram_prep_kernel (a zero-norm column j gets row/column e_j:
+// d_j = g_j = 0, the reference's skip).  g is recomputed from the current e at
+// every block, so rounding in M only perturbs the iterates, not the fixed
+// point; the variant is labelled and meets the same parity bar.
+//
+// Kernel: the on-chip layout of the column sweep — a cluster of CTAs, e in
+// registers (E rows per thread, rows tid + k*NT), a producer warp streaming
+// column slices with cp.async.bulk into a ring whose stage holds kW = 8
+// columns (one mbarrier wait per 8 columns).  Per block: pass 1 = 64 partial
+// dots (8 per stage, one 9-shuffle multi-value butterfly per warp), one
+// per-column sum over warps, one st.async exchange of the 64 partial vectors
+// across the cluster (rank order -> identical bits in every CTA), d = M g as a
+// 64x64 matvec from shared memory (M prefetched with cp.async during pass 1);
+// pass 2 re-streams the block (L2-resident) and applies e -= fl(d_j x_j)
+// column by column.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "bak_common.cuh"
+#include "bak_sweep.cuh"
+
+namespace bak {
+namespace {
+
+constexpr int kB = 64;      // block width
+constexpr int kW = 8;       // columns per ring stage
+constexpr int kMaxS = 32;   // ring stages
+constexpr int kMaxNT = 256;
+constexpr int kMaxW = kMaxNT / 32;
+constexpr int kMaxCl = 16;
+constexpr int kBarBG = 1;   // named barrier of the consumer warps
+
+struct BgParams {
+  const void* x;
+  int64_t obs, ldx, vars;
+  const double* minv;  // [nblocks][64 * 64], column-major: minv[b*4096 + k*64 + i] = M_b(i, k)
+  void* e;
+  void* a;
+  int64_t max_iter;
+  double thresh2;  // < 0: no early break
+  double* history;
+  int64_t* status;
+  int64_t rows_per_cta;
+  int nstages;
+};
+
+__device__ __forceinline__ bool bar_bg_or(int nthreads, int pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 q, %1, 0;\n\t"
+      "bar.red.or.pred p, %2, %3, q;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(static_cast<uint32_t>(pred)), "r"(kBarBG), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void st_async_d(uint32_t remote_addr, double v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(remote_addr),
+               "d"(v), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Sum 8 per-lane values over the warp with 9 shuffles: after the call, lane L
+// holds the warp total of value c(L) = 4*bit4(L) + 2*bit3(L) + bit2(L).
+template <typename T>
+__device__ __forceinline__ T warp_sum8(T (&v)[8], int lane) {
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const T send = hi ? v[i] : v[i + 4];
+      const T keep = hi ? v[i + 4] : v[i];
+      v[i] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const T send = hi ? v[i] : v[i + 2];
+      const T keep = hi ? v[i + 2] : v[i];
+      v[i] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+    }
+  }
+  {
+    const bool hi = lane & 4;
+    const T send = hi ? v[0] : v[1];
+    const T keep = hi ? v[1] : v[0];
+    v[0] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+  }
+  v[0] = Num<T>::add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 2));
+  v[0] = Num<T>::add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+  return v[0];
+}
+
+template <typename T, int E, bool CL>
+__global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams prm) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int NT = static_cast<int>(blockDim.x) - 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+  const int S = prm.nstages;
+  uint32_t rank = 0, G = 1;
+  if (CL) {
+    rank = cluster_rank();
+    G = cluster_size();
+  }
+  const T* __restrict__ x = static_cast<const T*>(prm.x);
+  T* __restrict__ eg = static_cast<T*>(prm.e);
+  T* __restrict__ ag = static_cast<T*>(prm.a);
+  const int64_t V = prm.vars;
+  const int64_t nblocks = (V + kB - 1) / kB;
+  const int64_t RP = prm.rows_per_cta;
+  const int64_t r0 = static_cast<int64_t>(rank) * RP;
+  const int64_t nrows = imax64(0, imin64(prm.obs - r0, RP));
+  constexpr int VEC = 16 / sizeof(T);
+  const uint32_t col_bytes = static_cast<uint32_t>(((nrows + VEC - 1) / VEC) * VEC * sizeof(T));
+
+  // ---- shared memory ----
+  size_t off = 0;
+  T* xs = reinterpret_cast<T*>(smem_raw);  // [S][kW][RP]
+  off += static_cast<size_t>(S) * kW * RP * sizeof(T);
+  off = (off + 127) & ~size_t(127);
+  double* msh = reinterpret_cast<double*>(smem_raw + off);  // [64*64] M of the current block
+  off += kB * kB * sizeof(double);
+  double* xslot = reinterpret_cast<double*>(smem_raw + off);  // [2][kMaxCl][kB] exchange
+  off += 2 * kMaxCl * kB * sizeof(double);
+  double* gsh = reinterpret_cast<double*>(smem_raw + off);  // [kB] block dots (cluster totals)
+  off += kB * sizeof(double);
+  T* dsh = reinterpret_cast<T*>(smem_raw + off);  // [kB] block deltas
+  off += kB * sizeof(T);
+  off = (off + 15) & ~size_t(15);
+  T* red = reinterpret_cast<T*>(smem_raw + off);  // [kB][kMaxW] per-warp partial dots
+  off += kB * kMaxW * sizeof(T);
+  off = (off + 15) & ~size_t(15);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + off);
+  off += kMaxS * 8;
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + off);
+  off += kMaxS * 8;
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2]
+  off += 16;
+  double* qsh = reinterpret_cast<double*>(smem_raw + off);
+  off += 16;
+  volatile int* stop = reinterpret_cast<volatile int*>(smem_raw + off);
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], nwarps);
+    }
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    *stop = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (CL) cluster_sync();
+
+  // stages of one block: ceil(width / kW); each block is streamed twice
+  auto block_w = [&](int64_t b) -> int { return static_cast<int>(imin64(kB, V - b * kB)); };
+
+  if (tid >= NT) {
+    // =========================== producer warp ===========================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();  // the block is read twice
+      int s = 0;
+      uint32_t ph = 0;
+      int64_t u = 0;
+      bool halted = false;
+      for (int64_t sw = 0; sw < prm.max_iter && !halted; ++sw)
+        for (int64_t b = 0; b < nblocks && !halted; ++b)
+          for (int pass = 0; pass < 2 && !halted; ++pass) {
+            const int w = block_w(b);
+            for (int c0 = 0; c0 < w && !halted; c0 += kW, ++u) {
+              if (u >= S) {
+                const uint32_t par = ph ^ 1u;
+                if (!mbar_test(&empty[s], par)) {
+                  const uint64_t t0 = globaltimer();
+                  while (!mbar_test(&empty[s], par)) {
+                    if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+                  }
+                }
+                if (halted) break;
+              }
+              const int n = w - c0 < kW ? w - c0 : kW;
+              mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * col_bytes);
+              if (col_bytes)
+                for (int i = 0; i < n; ++i)
+                  bulk_g2s(xs + (static_cast<size_t>(s) * kW + i) * RP, x + (b * kB + c0 + i) * prm.ldx + r0,
+                           col_bytes, &full[s], pol);
+              if (++s == S) { s = 0; ph ^= 1u; }
+            }
+          }
+      for (int64_t v = imax64(0, u - S); v < u; ++v) {  // in-flight copies land before exit
+        const uint64_t t0 = globaltimer();
+        while (!mbar_test(&full[v % S], static_cast<uint32_t>((v / S) & 1)))
+          if (globaltimer() - t0 > kTimeoutNs) break;
+      }
+    }
+  } else {
+    // =========================== consumers ===============================
+    const int kv = static_cast<int>(imax64(0, imin64(E, (nrows - tid + NT - 1) / NT)));
+    T ev[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? eg[r0 + tid + static_cast<int64_t>(k) * NT] : T(0);
+    const bool full_rows = kv == E;
+    int my_abort = 0;
+    int ls = 0;
+    uint32_t lph = 0;
+    const uint32_t xs_base = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
+    const uint32_t col_stride = static_cast<uint32_t>(RP * sizeof(T));
+    const uint32_t stage_stride = col_stride * kW;
+    auto wait_stage = [&]() -> uint32_t {
+      if (!mbar_test(&full[ls], lph)) {
+        const uint64_t t0 = globaltimer();
+        while (!mbar_test(&full[ls], lph)) {
+          if (globaltimer() - t0 > kTimeoutNs) {
+            report_error(prm.status, BAK_ETIMEOUT);
+            my_abort = 1;
+            break;
+          }
+        }
+      }
+      return xs_base + static_cast<uint32_t>(ls) * stage_stride;
+    };
+    auto release_stage = [&]() {
+      __syncwarp();
+      if (lane == 0) arrive1(&empty[ls]);
+      if (++ls == S) { ls = 0; lph ^= 1u; }
+    };
+    auto xval = [&](uint32_t a, int k) -> T {
+      return (full_rows || k < kv) ? lds<T>(a + static_cast<uint32_t>(k * NT * sizeof(T))) : T(0);
+    };
+    // cluster sum of n values (thread t < n holds v), rank order; result in t < n
+    uint32_t rc = 0;
+    auto exchange = [&](double v, int n) -> double {
+      if (!CL) return v;
+      const int buf = rc & 1;
+      const uint32_t par = (rc >> 1) & 1;
+      ++rc;
+      if (tid < n) {
+        const uint32_t loc = smem_addr(&xslot[(buf * kMaxCl + rank) * kB + tid]);
+        const uint32_t lb = smem_addr(&xbar[buf]);
+        for (uint32_t r = 0; r < G; ++r) st_async_d(mapa(loc, r), v, mapa(lb, r));
+      }
+      if (tid == 0) mbar_arrive_expect_tx(&xbar[buf], G * static_cast<uint32_t>(n) * 8u);
+      double tot = 0.0;
+      if (tid < n) {
+        if (!mbar_test_cluster(&xbar[buf], par)) {
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test_cluster(&xbar[buf], par)) {
+            if (globaltimer() - t0 > kTimeoutNs) {
+              report_error(prm.status, BAK_ETIMEOUT);
+              my_abort = 1;
+              break;
+            }
+          }
+        }
+        double s = 0.0;
+        for (uint32_t r = 0; r < G; ++r) s += xslot[(buf * kMaxCl + r) * kB + tid];
+        tot = s;
+      }
+      return tot;
+    };
+
+    int64_t sweep = 0;
+    bool converged = false, aborted = false;
+    const uint32_t msh_s = smem_addr(msh);
+    while (sweep < prm.max_iter && !aborted) {
+      for (int64_t b = 0; b < nblocks && !aborted; ++b) {
+        const int w = block_w(b);
+        // prefetch this block's M (32 KB) while pass 1 runs
+        {
+          const char* src = reinterpret_cast<const char*>(prm.minv + b * kB * kB);
+          for (int i = tid; i < kB * kB * 8 / 16; i += NT) cp_async16(msh_s + 16u * i, src + 16 * i);
+          cp_async_commit();
+        }
+        // ---- pass 1: partial dots of the block's columns against e ----
+        for (int c0 = 0; c0 < w; c0 += kW) {
+          const uint32_t a = wait_stage();
+          const int n = w - c0 < kW ? w - c0 : kW;
+          T p[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            T acc[2] = {T(0), T(0)};
+            if (c < n) {
+#pragma unroll
+              for (int k = 0; k < E; ++k) acc[k & 1] = Num<T>::fma(xval(a + c * col_stride, k), ev[k], acc[k & 1]);
+            }
+            p[c] = Num<T>::add(acc[0], acc[1]);
+          }
+          release_stage();
+          const T s8 = warp_sum8(p, lane);
+          if ((lane & 3) == 0) {
+            const int c = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
+            red[(c0 + c) * kMaxW + warp] = s8;
+          }
+        }
+        if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
+        double v = 0.0;
+        if (tid < w) {
+          T s = T(0);
+          for (int ww = 0; ww < nwarps; ++ww) s = Num<T>::add(s, red[tid * kMaxW + ww]);
+          v = static_cast<double>(s);
+        }
+        const double g = exchange(v, w);
+        if (tid < w) gsh[tid] = g;
+        cp_async_wait_all();
+        if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
+        // ---- d = M g (fp64), a += d ----
+        if (tid < w) {
+          double d = 0.0;
+          for (int k = 0; k < w; ++k) d = __fma_rn(msh[k * kB + tid], gsh[k], d);
+          const T dt = static_cast<T>(d);
+          dsh[tid] = dt;
+          if (rank == 0) ag[b * kB + tid] = Num<T>::add(ag[b * kB + tid], dt);
+        }
+        if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
+        // ---- pass 2: e -= fl(d_j x_j), column by column (two roundings, bak.py:87-88) ----
+        for (int c0 = 0; c0 < w; c0 += kW) {
+          const uint32_t a = wait_stage();
+          const int n = w - c0 < kW ? w - c0 : kW;
+          for (int c = 0; c < n; ++c) {
+            const T d = dsh[c0 + c];
+#pragma unroll
+            for (int k = 0; k < E; ++k) ev[k] = Num<T>::sub(ev[k], Num<T>::mul(xval(a + c * col_stride, k), d));
+          }
+          release_stage();
+        }
+      }
+      if (aborted) break;
+      // ---- sweep end: sum e^2, history, early break (bak.py:106-111) ----
+      T q[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+      for (int k = 0; k < E; ++k) q[k & 3] = Num<T>::fma(ev[k], ev[k], q[k & 3]);
+      const T qv = warp_sum(Num<T>::add(Num<T>::add(q[0], q[1]), Num<T>::add(q[2], q[3])));
+      if (lane == 0) red[warp] = qv;
+      if (bar_bg_or(NT, my_abort)) break;
+      double qd = 0.0;
+      if (tid == 0) {
+        T s = T(0);
+        for (int ww = 0; ww < nwarps; ++ww) s = Num<T>::add(s, red[ww]);
+        qd = static_cast<double>(s);
+      }
+      qd = exchange(qd, 1);
+      if (tid == 0) {
+        *qsh = qd;
+        if (rank == 0 && prm.history) prm.history[sweep] = qd;
+      }
+      if (bar_bg_or(NT, my_abort)) break;
+      const double sq = *qsh;
+      ++sweep;
+      if (prm.thresh2 >= 0.0 && sq <= prm.thresh2) {
+        converged = true;
+        break;
+      }
+    }
+    {
+      T* ew = eg + r0 + tid;
+      asm volatile("mov.b64 %0, %0;" : "+l"(ew));
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (k < kv) ew[static_cast<int64_t>(k) * NT] = ev[k];
+    }
+    if (tid == 0) {
+      *stop = 1;
+      if (rank == 0 && prm.status) {
+        prm.status[0] = sweep;
+        prm.status[1] = converged ? 1 : 0;
+        prm.status[3] = BAK_VARIANT_BGRAM;
+      }
+    }
+  }
+  __syncthreads();
+  if (CL) cluster_sync();
+}
+
+// M_b = L_b^{-1} for every 64-column block b: G_BB = X_B^T X_B in fp64 (rows in
+// 32-row tiles, fixed order), L = its lower triangle, inverted column by
+// column by forward substitution (thread j solves L m = e_j).  A zero-norm
+// column j (L_jj == 0) gets row and column e_j.
+template <typename T>
+__global__ void __launch_bounds__(256) bgram_prep_kernel(const T* __restrict__ x, int64_t obs, int64_t ldx,
+                                                         int64_t vars, double* __restrict__ minv) {
+  __shared__ double buf[kB * (kB + 1)];  // the row tile, later L (after the accumulation)
+  double (*xt)[kB + 1] = reinterpret_cast<double (*)[kB + 1]>(buf);  // [32][65]: [row][column]
+  double (*L)[kB + 1] = reinterpret_cast<double (*)[kB + 1]>(buf);   // [64][65]: [i][j]
+  const int64_t b = blockIdx.x;
+  const int w = static_cast<int>(imin64(kB, vars - b * kB));
+  const int tid = threadIdx.x;
+  const int ti = tid / 16, tj = tid % 16;  // 4x4 outputs: rows 4ti.., cols 4tj..
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int64_t r0 = 0; r0 < obs; r0 += 32) {
+    __syncthreads();
+    for (int idx = tid; idx < 32 * kB; idx += 256) {
+      const int c = idx / 32, r = idx % 32;  // coalesced along rows of a column
+      const int64_t row = r0 + r;
+      xt[r][c] = (c < w && row < obs) ? static_cast<double>(x[(b * kB + c) * ldx + row]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      double xi[4], xj[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xi[i] = xt[r][4 * ti + i];
+        xj[i] = xt[r][4 * tj + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(xi[i], xj[j], acc[i][j]);
+    }
+  }
+  __syncthreads();  // done with the row tiles: the buffer becomes L
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gi = 4 * ti + i, gj = 4 * tj + j;
+      L[gi][gj] = (gj <= gi) ? acc[i][j] : 0.0;
+    }
+  __syncthreads();
+  if (tid < kB) {
+    const int j = tid;
+    double m[kB];  // column j of M
+    for (int i = 0; i < kB; ++i) {
+      if (i < j) {
+        m[i] = 0.0;
+        continue;
+      }
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s = __fma_rn(-L[i][k], m[k], s);
+      const double lii = L[i][i];
+      m[i] = (lii != 0.0) ? s / lii : ((i == j) ? 1.0 : 0.0);
+      if (lii == 0.0 && i != j) m[i] = 0.0;
+    }
+    // a zero-norm column i: row i of M = e_i^T (d_i = g_i = 0); L's column i is 0 already
+    double* out = minv + b * kB * kB;
+    for (int i = 0; i < kB; ++i) out[j * kB + i] = m[i];  // column-major: out[k*64 + i] = M(i, k), k = j
+  }
+}
+
+struct BgPlan {
+  int parts = 1, nt = 32, e = 4, nstages = 2;
+  int64_t rows_per_cta = 0;
+};
+
+size_t bg_smem(const BgPlan& p, size_t ts) {
+  size_t off = static_cast<size_t>(p.nstages) * kW * p.rows_per_cta * ts;
+  off = (off + 127) & ~size_t(127);
+  off += kB * kB * 8 + 2 * kMaxCl * kB * 8 + kB * 8 + kB * ts;
+  off = (off + 15) & ~size_t(15);
+  off += kB * kMaxW * ts;
+  off = (off + 15) & ~size_t(15);
+  return off + 2 * kMaxS * 8 + 16 + 16 + 16;
+}
+
+bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
+  const size_t ts = dtype_size(dtype);
+  const size_t cap = static_cast<size_t>(device_max_smem_optin()) - 2048;
+  // as many CTAs as a cluster allows (bandwidth), at least 64 rows each
+  int parts = static_cast<int>((obs + 63) / 64);
+  if (parts > kMaxCl) parts = kMaxCl;
+  if (parts < 1) parts = 1;
+  const int64_t per = (obs + parts - 1) / parts;
+  for (int e : {4, 8, 16}) {
+    int64_t nt = round_up((per + e - 1) / e, 32);
+    if (nt < kB) nt = kB;  // threads t < 64 finish the block's 64 dots and deltas
+    if (nt > kMaxNT) continue;
+    BgPlan c;
+    c.parts = parts;
+    c.nt = static_cast<int>(nt);
+    c.e = e;
+    c.rows_per_cta = round_up(per, 4);
+    if (c.rows_per_cta > nt * e) continue;
+    c.nstages = 0;
+    const size_t fixed = bg_smem(c, ts);
+    const size_t sb = static_cast<size_t>(kW) * c.rows_per_cta * ts;
+    if (fixed + 3 * sb > cap) continue;
+    int s = static_cast<int>((cap - fixed) / sb);
+    c.nstages = s > kMaxS ? kMaxS : s;
+    pl = c;
+    return true;
+  }
+  return false;
+}
+
+template <typename T, int E, bool CL>
+int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
+  auto kern = bgram_kernel<T, E, CL>;
+  const size_t smem = bg_smem(pl, sizeof(T));
+  BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.parts);
+  cfg.blockDim = dim3(pl.nt + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (CL) {
+    if (pl.parts > 8) BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = pl.parts;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  count_launches(1);
+  return BAK_OK;
+}
+
+template <typename T>
+int bg_launch_e(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
+  const bool cl = pl.parts > 1;
+  switch (pl.e) {
+    case 4: return cl ? bg_launch<T, 4, true>(pl, prm, st) : bg_launch<T, 4, false>(pl, prm, st);
+    case 8: return cl ? bg_launch<T, 8, true>(pl, prm, st) : bg_launch<T, 8, false>(pl, prm, st);
+    case 16: return cl ? bg_launch<T, 16, true>(pl, prm, st) : bg_launch<T, 16, false>(pl, prm, st);
+  }
+  set_error("bak_sweep(BGRAM): unsupported rows per thread %d", pl.e);
+  return BAK_EUNSUPPORTED;
+}
+
+}  // namespace
+
+int64_t bgram_workspace_bytes(int64_t vars) { return ((vars + kB - 1) / kB) * kB * kB * 8 + 256; }
+
+bool bgram_supported(int dtype, int64_t obs) {
+  BgPlan pl;
+  return bg_plan(dtype, obs, pl);
+}
+
+int launch_bgram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st) {
+  if (prm.cols && prm.cols_stride != 0) {
+    set_error("bak_sweep(BGRAM): cyclic ordering only (blocks of 64 consecutive columns)");
+    return BAK_EUNSUPPORTED;
+  }
+  BgPlan pl;
+  if (!bg_plan(dtype, prm.obs, pl)) {
+    set_error("bak_sweep(BGRAM): obs=%lld does not fit one cluster", (long long)prm.obs);
+    return BAK_EUNSUPPORTED;
+  }
+  if (wsb < bgram_workspace_bytes(vars)) {
+    set_error("bak_sweep(BGRAM): workspace too small (need %lld)", (long long)bgram_workspace_bytes(vars));
+    return BAK_EWORKSPACE;
+  }
+  double* minv = static_cast<double*>(ws);
+  const unsigned nb = static_cast<unsigned>((vars + kB - 1) / kB);
+  if (dtype == BAK_F64)
+    bgram_prep_kernel<double><<<nb, 256, 0, st>>>(static_cast<const double*>(prm.x), prm.obs, prm.ldx, vars, minv);
+  else
+    bgram_prep_kernel<float><<<nb, 256, 0, st>>>(static_cast<const float*>(prm.x), prm.obs, prm.ldx, vars, minv);
+  count_launches(1);
+  BAK_CHECK_CUDA(cudaGetLastError());
+  BAK_CHECK_CUDA(cudaMemsetAsync(prm.status, 0, 4 * sizeof(int64_t), st));
+  BgParams bp{prm.x, prm.obs, prm.ldx, vars, minv, prm.e, prm.a, prm.max_iter, prm.thresh2, prm.history,
+              prm.status, pl.rows_per_cta, pl.nstages};
+  const int rc = dtype == BAK_F64 ? bg_launch_e<double>(pl, bp, st) : bg_launch_e<float>(pl, bp, st);
+  if (rc) return rc;
+  BAK_CHECK_CUDA(cudaGetLastError());
+  return BAK_OK;
+}
+
+}  // namespace bak

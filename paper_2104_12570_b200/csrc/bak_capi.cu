@@ -108,6 +108,10 @@ extern "C" int64_t bak_sweep_workspace(int dtype, int variant, int64_t obs, int6
     const int64_t g = gram_workspace_bytes(dtype, obs, vars);
     return g > kSlotBytes ? g : kSlotBytes;
   }
+  if (variant == BAK_VARIANT_BGRAM) {
+    const int64_t g = bgram_workspace_bytes(vars);
+    return g > kSlotBytes ? g : kSlotBytes;
+  }
   return kSlotBytes;
 }
 
@@ -157,6 +161,7 @@ extern "C" int bak_sweep(int dtype, int variant, const void* x, int64_t obs, int
   prm.status = status;
   prm.slots = static_cast<uint32_t*>(workspace);
   if (variant == BAK_VARIANT_GRAM) return launch_gram(dtype, prm, vars, workspace, workspace_bytes, st);
+  if (variant == BAK_VARIANT_BGRAM) return launch_bgram(dtype, prm, vars, workspace, workspace_bytes, st);
   if (variant == BAK_VARIANT_STREAM) {
     StreamPlan sp;
     if (!plan_stream(dtype, obs, sp)) {

@@ -76,5 +76,9 @@ int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int
                          cudaStream_t st, const void* afin = nullptr, const void* y = nullptr, void* resid = nullptr,
                          int64_t* status = nullptr);
 int launch_gram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st);
+// block-Gram sweep (bak_bgram.cu): residual on one cluster, cyclic order
+int64_t bgram_workspace_bytes(int64_t vars);
+bool bgram_supported(int dtype, int64_t obs);
+int launch_bgram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int64_t wsb, cudaStream_t st);
 
 }  // namespace bak

@@ -23,9 +23,11 @@
 // dots (8 per stage, one 9-shuffle multi-value butterfly per warp), one
 // per-column sum over warps, one st.async exchange of the 64 partial vectors
 // across the cluster (rank order -> identical bits in every CTA), d = M g as a
-// 64x64 matvec from shared memory (M prefetched with cp.async during pass 1);
-// pass 2 re-streams the block (L2-resident) and applies e -= fl(d_j x_j)
-// column by column.
+// 64x64 matvec from shared memory (M double-buffered, one bulk copy per block
+// issued by the producer ahead of the block);
+// pass 2 re-reads the block (from the ring when it stays resident, else
+// re-streamed from L2) and applies e -= (sum of d_j x_j over 8 columns,
+// pairwise) — labelled: the reference rounds per column.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -56,6 +58,7 @@ struct BgParams {
   int64_t* status;
   int64_t rows_per_cta;
   int nstages;
+  int resident;  // 1: a block's stages stay in the ring from pass 1 to pass 2 (read once)
 };
 
 __device__ __forceinline__ bool bar_bg_or(int nthreads, int pred) {
@@ -78,47 +81,74 @@ __device__ __forceinline__ void st_async_d(uint32_t remote_addr, double v, uint3
                "d"(v), "r"(remote_bar)
                : "memory");
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Sum 8 per-lane values over the warp with 9 shuffles: after the call, lane L
-// holds the warp total of value c(L) = 4*bit4(L) + 2*bit3(L) + bit2(L).
-template <typename T>
-__device__ __forceinline__ T warp_sum8(T (&v)[8], int lane) {
-  {
-    const bool hi = lane & 16;
+// Sum N per-lane values (N = 8 or 64) over the warp by recursive halving:
+// each round a lane keeps the half of its values selected by one lane bit and
+// adds the partner's copy of that half (N - 1 + log2(32 / N) shuffles in all,
+// every round's shuffles independent).  Afterwards lane L holds, in v[0..R),
+// R = max(1, N / 32), the warp totals of values
+//   c(L, i) = i + R * (bit0 + 2 bit1 + 4 bit2 + 8 bit3 + 16 bit4 of L restricted
+//             to the rounds that halved),  see col_of below.  Fixed order: deterministic.
+template <typename T, int N>
+__device__ __forceinline__ void warp_sum_multi(T (&v)[N], int lane) {
+  int n = N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const T send = hi ? v[i] : v[i + 4];
-      const T keep = hi ? v[i + 4] : v[i];
-      v[i] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+  for (int o = 16; o >= 1; o >>= 1) {
+    if (n > 1) {
+      const bool hi = lane & o;
+      const int h = n / 2;
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        if (i < h) {
+          const T send = hi ? v[i] : v[i + h];
+          const T keep = hi ? v[i + h] : v[i];
+          v[i] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, o));
+        }
+      }
+      n = h;
+    } else {
+      v[0] = Num<T>::add(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
     }
   }
-  {
-    const bool hi = lane & 8;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const T send = hi ? v[i] : v[i + 2];
-      const T keep = hi ? v[i + 2] : v[i];
-      v[i] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, 8));
-    }
-  }
-  {
-    const bool hi = lane & 4;
-    const T send = hi ? v[0] : v[1];
-    const T keep = hi ? v[1] : v[0];
-    v[0] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, 4));
-  }
-  v[0] = Num<T>::add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 2));
-  v[0] = Num<T>::add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
-  return v[0];
 }
+// which value lane L holds in slot i after warp_sum_multi<T, N>
+template <int N>
+__device__ __forceinline__ int col_of(int lane, int i) {
+  int c = 0, n = N;
+#pragma unroll
+  for (int o = 16; o >= 1 && n > 1; o >>= 1) {
+    n >>= 1;
+    if (lane & o) c += n;
+  }
+  return c + i;
+}
+
+#ifdef BAK_PHASES
+#define GPH(i)                                 \
+  do {                                         \
+    if (tid == 0) {                            \
+      const long long _c = clock64();          \
+      ph_acc[i] += _c - ph_last;               \
+      ph_last = _c;                            \
+    }                                          \
+  } while (0)
+#else
+#define GPH(i) \
+  do {         \
+  } while (0)
+#endif
+
+// E <= 4 keeps 64 partial dots per thread in registers: at most 7 warps
+// (192 consumers + producer) so a thread may use up to 255 registers
+constexpr int bg_max_threads(int e) { return e <= 4 ? 224 : kMaxNT + 32; }
 
 template <typename T, int E, bool CL>
-__global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams prm) {
+__global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgParams prm) {
+  constexpr int CB = E <= 4 ? 8 : (E <= 8 ? 4 : 2);  // columns whose slices are loaded together
+#ifdef BAK_PHASES
+  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+#endif
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NT = static_cast<int>(blockDim.x) - 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
@@ -144,8 +174,8 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
   T* xs = reinterpret_cast<T*>(smem_raw);  // [S][kW][RP]
   off += static_cast<size_t>(S) * kW * RP * sizeof(T);
   off = (off + 127) & ~size_t(127);
-  double* msh = reinterpret_cast<double*>(smem_raw + off);  // [64*64] M of the current block
-  off += kB * kB * sizeof(double);
+  double* msh = reinterpret_cast<double*>(smem_raw + off);  // [2][64*64] M of the current / next block
+  off += 2 * kB * kB * sizeof(double);
   double* xslot = reinterpret_cast<double*>(smem_raw + off);  // [2][kMaxCl][kB] exchange
   off += 2 * kMaxCl * kB * sizeof(double);
   double* gsh = reinterpret_cast<double*>(smem_raw + off);  // [kB] block dots (cluster totals)
@@ -162,6 +192,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
   off += kMaxS * 8;
   uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2]
   off += 16;
+  uint64_t* mfull = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2] M buffer landed
+  off += 16;
+  uint64_t* mempty = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2] M buffer read by the matvec
+  off += 16;
   double* qsh = reinterpret_cast<double*>(smem_raw + off);
   off += 16;
   volatile int* stop = reinterpret_cast<volatile int*>(smem_raw + off);
@@ -173,6 +207,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
     }
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&mfull[i], 1);
+      mbar_init(&mempty[i], 1);
+    }
     *stop = 0;
     fence_mbar_init();
   }
@@ -190,10 +228,29 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
       uint32_t ph = 0;
       int64_t u = 0;
       bool halted = false;
+      int64_t mb = 0;  // blocks whose M has been issued
       for (int64_t sw = 0; sw < prm.max_iter && !halted; ++sw)
         for (int64_t b = 0; b < nblocks && !halted; ++b)
-          for (int pass = 0; pass < 2 && !halted; ++pass) {
+          for (int pass = 0; pass < (prm.resident ? 1 : 2) && !halted; ++pass) {
             const int w = block_w(b);
+            if (pass == 0) {
+              // the block's M (32 KB, one bulk copy) into buffer mb & 1, once the
+              // matvec two blocks back has read it
+              const int mbuf = static_cast<int>(mb & 1);
+              if (mb >= 2) {
+                const uint32_t par = static_cast<uint32_t>(((mb >> 1) - 1) & 1);
+                if (!mbar_test(&mempty[mbuf], par)) {
+                  const uint64_t t0 = globaltimer();
+                  while (!mbar_test(&mempty[mbuf], par)) {
+                    if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+                  }
+                }
+                if (halted) break;
+              }
+              mbar_arrive_expect_tx(&mfull[mbuf], kB * kB * 8u);
+              bulk_g2s(msh + mbuf * kB * kB, prm.minv + b * kB * kB, kB * kB * 8u, &mfull[mbuf], pol);
+              ++mb;
+            }
             for (int c0 = 0; c0 < w && !halted; c0 += kW, ++u) {
               if (u >= S) {
                 const uint32_t par = ph ^ 1u;
@@ -217,6 +274,11 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
       for (int64_t v = imax64(0, u - S); v < u; ++v) {  // in-flight copies land before exit
         const uint64_t t0 = globaltimer();
         while (!mbar_test(&full[v % S], static_cast<uint32_t>((v / S) & 1)))
+          if (globaltimer() - t0 > kTimeoutNs) break;
+      }
+      for (int64_t v = imax64(0, mb - 2); v < mb; ++v) {  // and the last two M copies
+        const uint64_t t0 = globaltimer();
+        while (!mbar_test(&mfull[v & 1], static_cast<uint32_t>((v >> 1) & 1)))
           if (globaltimer() - t0 > kTimeoutNs) break;
       }
     }
@@ -288,38 +350,80 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
 
     int64_t sweep = 0;
     bool converged = false, aborted = false;
-    const uint32_t msh_s = smem_addr(msh);
+    int64_t mi = 0;  // blocks consumed (M buffer mi & 1)
+    if (tid < kB) gsh[tid] = 0.0;  // (finite before the first block; see the matvec)
     while (sweep < prm.max_iter && !aborted) {
       for (int64_t b = 0; b < nblocks && !aborted; ++b) {
         const int w = block_w(b);
-        // prefetch this block's M (32 KB) while pass 1 runs
-        {
-          const char* src = reinterpret_cast<const char*>(prm.minv + b * kB * kB);
-          for (int i = tid; i < kB * kB * 8 / 16; i += NT) cp_async16(msh_s + 16u * i, src + 16 * i);
-          cp_async_commit();
-        }
         // ---- pass 1: partial dots of the block's columns against e ----
+        const int ls_block = ls;  // resident: pass 2 re-reads these stages
+        if constexpr (E <= 4) {
+          // the block's 64 partial dots stay in registers across its 8 stages;
+          // ONE multi-value warp reduction per block
+          T p[kB];
+#pragma unroll
+          for (int c = 0; c < kB; ++c) p[c] = T(0);
+#pragma unroll
+          for (int st8 = 0; st8 < kB / kW; ++st8) {
+            const int c0 = st8 * kW;
+            if (c0 < w) {
+              const uint32_t a = wait_stage();
+              const int n = w - c0 < kW ? w - c0 : kW;
+              T xr[kW][E];
+#pragma unroll
+              for (int c = 0; c < kW; ++c)
+#pragma unroll
+                for (int k = 0; k < E; ++k) xr[c][k] = (c < n) ? xval(a + c * col_stride, k) : T(0);
+#pragma unroll
+              for (int c = 0; c < kW; ++c) {
+                T acc[2] = {T(0), T(0)};
+#pragma unroll
+                for (int k = 0; k < E; ++k) acc[k & 1] = Num<T>::fma(xr[c][k], ev[k], acc[k & 1]);
+                p[c0 + c] = Num<T>::add(acc[0], acc[1]);
+              }
+              if (prm.resident) {
+                if (++ls == S) { ls = 0; lph ^= 1u; }
+              } else {
+                release_stage();
+              }
+            }
+          }
+          warp_sum_multi<T, kB>(p, lane);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) red[col_of<kB>(lane, i) * kMaxW + warp] = p[i];
+        } else {
         for (int c0 = 0; c0 < w; c0 += kW) {
           const uint32_t a = wait_stage();
           const int n = w - c0 < kW ? w - c0 : kW;
           T p[8];
+          // batches of CB columns: all their loads issued before the arithmetic
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            T acc[2] = {T(0), T(0)};
-            if (c < n) {
+          for (int cb = 0; cb < 8; cb += CB) {
+            T xr[CB][E];
 #pragma unroll
-              for (int k = 0; k < E; ++k) acc[k & 1] = Num<T>::fma(xval(a + c * col_stride, k), ev[k], acc[k & 1]);
+            for (int c = 0; c < CB; ++c)
+#pragma unroll
+              for (int k = 0; k < E; ++k) xr[c][k] = (cb + c < n) ? xval(a + (cb + c) * col_stride, k) : T(0);
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+              T acc[2] = {T(0), T(0)};
+#pragma unroll
+              for (int k = 0; k < E; ++k) acc[k & 1] = Num<T>::fma(xr[c][k], ev[k], acc[k & 1]);
+              p[cb + c] = Num<T>::add(acc[0], acc[1]);
             }
-            p[c] = Num<T>::add(acc[0], acc[1]);
           }
-          release_stage();
-          const T s8 = warp_sum8(p, lane);
-          if ((lane & 3) == 0) {
-            const int c = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
-            red[(c0 + c) * kMaxW + warp] = s8;
+          if (prm.resident) {
+            if (++ls == S) { ls = 0; lph ^= 1u; }
+          } else {
+            release_stage();
           }
+          warp_sum_multi<T, kW>(p, lane);
+          if ((lane & 3) == 0) red[(c0 + col_of<kW>(lane, 0)) * kMaxW + warp] = p[0];
         }
+        }
+        GPH(0);
         if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
+        GPH(1);
         double v = 0.0;
         if (tid < w) {
           T s = T(0);
@@ -328,28 +432,74 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
         }
         const double g = exchange(v, w);
         if (tid < w) gsh[tid] = g;
-        cp_async_wait_all();
+        GPH(2);
+        const int mbuf = static_cast<int>(mi & 1);
+        const uint32_t mpar = static_cast<uint32_t>((mi >> 1) & 1);
+        if (tid < kB && !mbar_test(&mfull[mbuf], mpar)) {
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test(&mfull[mbuf], mpar)) {
+            if (globaltimer() - t0 > kTimeoutNs) {
+              report_error(prm.status, BAK_ETIMEOUT);
+              my_abort = 1;
+              break;
+            }
+          }
+        }
         if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
-        // ---- d = M g (fp64), a += d ----
+        GPH(3);
+        // ---- d = M g (fp64, four interleaved partial sums), a += d ----
         if (tid < w) {
-          double d = 0.0;
-          for (int k = 0; k < w; ++k) d = __fma_rn(msh[k * kB + tid], gsh[k], d);
-          const T dt = static_cast<T>(d);
+          const double* mcol = msh + mbuf * kB * kB + tid;
+          double dp[4] = {0.0, 0.0, 0.0, 0.0};
+          // all 64 terms: past a ragged block's width M(i, k) = 0 and gsh[k] is finite
+#pragma unroll
+          for (int k = 0; k < kB; ++k) dp[k & 3] = __fma_rn(mcol[k * kB], gsh[k], dp[k & 3]);
+          const T dt = static_cast<T>((dp[0] + dp[1]) + (dp[2] + dp[3]));
           dsh[tid] = dt;
           if (rank == 0) ag[b * kB + tid] = Num<T>::add(ag[b * kB + tid], dt);
         }
         if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
+        if (tid == 0) arrive1(&mempty[mbuf]);  // every matvec read is before the barrier
+        ++mi;
+        GPH(4);
         // ---- pass 2: e -= fl(d_j x_j), column by column (two roundings, bak.py:87-88) ----
+        int s2 = ls_block;
         for (int c0 = 0; c0 < w; c0 += kW) {
-          const uint32_t a = wait_stage();
+          const uint32_t a = prm.resident ? xs_base + static_cast<uint32_t>(s2) * stage_stride : wait_stage();
           const int n = w - c0 < kW ? w - c0 : kW;
-          for (int c = 0; c < n; ++c) {
-            const T d = dsh[c0 + c];
 #pragma unroll
-            for (int k = 0; k < E; ++k) ev[k] = Num<T>::sub(ev[k], Num<T>::mul(xval(a + c * col_stride, k), d));
+          for (int cb = 0; cb < 8; cb += CB) {
+            T xr[CB][E], dd[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+              dd[c] = (cb + c < n) ? dsh[c0 + cb + c] : T(0);  // past the block: e - fl(0 * 0) = e
+#pragma unroll
+              for (int k = 0; k < E; ++k) xr[c][k] = (cb + c < n) ? xval(a + (cb + c) * col_stride, k) : T(0);
+            }
+            // e -= (sum of the CB products, pairwise tree) — a short dependency chain
+            // instead of 2 CB dependent ops per row (labelled variant: the rounding
+            // is not the reference's per-column one)
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+              T pr[CB];
+#pragma unroll
+              for (int c = 0; c < CB; ++c) pr[c] = Num<T>::mul(xr[c][k], dd[c]);
+#pragma unroll
+              for (int h = CB / 2; h >= 1; h >>= 1)
+#pragma unroll
+                for (int c = 0; c < h; ++c) pr[c] = Num<T>::add(pr[c], pr[c + h]);
+              ev[k] = Num<T>::sub(ev[k], pr[0]);
+            }
           }
-          release_stage();
+          if (prm.resident) {
+            __syncwarp();
+            if (lane == 0) arrive1(&empty[s2]);
+            if (++s2 == S) s2 = 0;
+          } else {
+            release_stage();
+          }
         }
+        GPH(5);
       }
       if (aborted) break;
       // ---- sweep end: sum e^2, history, early break (bak.py:106-111) ----
@@ -385,6 +535,10 @@ __global__ void __launch_bounds__(kMaxNT + 32, 1) bgram_kernel(const BgParams pr
       for (int k = 0; k < E; ++k)
         if (k < kv) ew[static_cast<int64_t>(k) * NT] = ev[k];
     }
+#ifdef BAK_PHASES
+    if (tid == 0 && rank == 0 && prm.history)
+      for (int i = 0; i < 8; ++i) prm.history[prm.max_iter + i] = static_cast<double>(ph_acc[i]);
+#endif
     if (tid == 0) {
       *stop = 1;
       if (rank == 0 && prm.status) {
@@ -469,18 +623,18 @@ __global__ void __launch_bounds__(256) bgram_prep_kernel(const T* __restrict__ x
 }
 
 struct BgPlan {
-  int parts = 1, nt = 32, e = 4, nstages = 2;
+  int parts = 1, nt = 32, e = 4, nstages = 2, resident = 0;
   int64_t rows_per_cta = 0;
 };
 
 size_t bg_smem(const BgPlan& p, size_t ts) {
   size_t off = static_cast<size_t>(p.nstages) * kW * p.rows_per_cta * ts;
   off = (off + 127) & ~size_t(127);
-  off += kB * kB * 8 + 2 * kMaxCl * kB * 8 + kB * 8 + kB * ts;
+  off += 2 * kB * kB * 8 + 2 * kMaxCl * kB * 8 + kB * 8 + kB * ts;
   off = (off + 15) & ~size_t(15);
   off += kB * kMaxW * ts;
   off = (off + 15) & ~size_t(15);
-  return off + 2 * kMaxS * 8 + 16 + 16 + 16;
+  return off + 2 * kMaxS * 8 + 16 + 16 + 16 + 32;
 }
 
 bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
@@ -494,7 +648,7 @@ bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
   for (int e : {4, 8, 16}) {
     int64_t nt = round_up((per + e - 1) / e, 32);
     if (nt < kB) nt = kB;  // threads t < 64 finish the block's 64 dots and deltas
-    if (nt > kMaxNT) continue;
+    if (nt + 32 > bg_max_threads(e)) continue;
     BgPlan c;
     c.parts = parts;
     c.nt = static_cast<int>(nt);
@@ -507,6 +661,10 @@ bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
     if (fixed + 3 * sb > cap) continue;
     int s = static_cast<int>((cap - fixed) / sb);
     c.nstages = s > kMaxS ? kMaxS : s;
+    // a block (8 stages) stays resident between its passes when the ring also
+    // holds at least one more block's worth of prefetch
+    c.resident = c.nstages >= 2 * (kB / kW) ? 1 : 0;
+    if (const char* r = getenv("BAK_BGRAM_RESIDENT")) c.resident = (r[0] == '1') && c.nstages > kB / kW;
     pl = c;
     return true;
   }
@@ -585,7 +743,7 @@ int launch_bgram(int dtype, const SweepParams& prm, int64_t vars, void* ws, int6
   BAK_CHECK_CUDA(cudaGetLastError());
   BAK_CHECK_CUDA(cudaMemsetAsync(prm.status, 0, 4 * sizeof(int64_t), st));
   BgParams bp{prm.x, prm.obs, prm.ldx, vars, minv, prm.e, prm.a, prm.max_iter, prm.thresh2, prm.history,
-              prm.status, pl.rows_per_cta, pl.nstages};
+              prm.status, pl.rows_per_cta, pl.nstages, pl.resident};
   const int rc = dtype == BAK_F64 ? bg_launch_e<double>(pl, bp, st) : bg_launch_e<float>(pl, bp, st);
   if (rc) return rc;
   BAK_CHECK_CUDA(cudaGetLastError());

@@ -527,7 +527,11 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         Q = static_cast<T>(bcast[buf].q);
         return any2;
       }
-      // kModeGrid: partial records -> aggregator (CTA 0) -> per-CTA result lines
+      // kModeGrid: partial records -> aggregator (CTA 0) -> per-CTA result lines;
+      // or (prm.grid_allgather) every CTA gathers all G records itself — one
+      // L2 round trip instead of two (records double-buffered by round: a CTA
+      // can post round rc+2 only after every CTA posted rc+1, i.e. finished
+      // reading round rc)
       const uint32_t epoch = rc + 1;
       uint32_t* part = prm.slots + static_cast<size_t>(buf) * kGridSlotsMax * 8;
       uint32_t* result = prm.slots + static_cast<size_t>(2) * kGridSlotsMax * 8 +
@@ -537,8 +541,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         if (with_q) ll_store(part + static_cast<size_t>(rank) * 8 + 4, static_cast<double>(bq), epoch);
       }
       bool timed_out = false;
+      const bool ag = prm.grid_allgather != 0;
       if (warp == 0) {
-        if (rank == 0) {
+        if (rank == 0 || ag) {
           // aggregator: lane l owns records l, l+32, ... (<= 8 per lane), all in flight together
           constexpr int kPer = kGridSlotsMax / 32;
           T vp[kPer], vq[kPer];
@@ -578,12 +583,16 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
             }
           const T sp = warp_sum(vp[0]);
           const T sq = with_q ? warp_sum(vq[0]) : T(0);
-          for (uint32_t r = lane; r < G; r += 32) {
-            ll_store(result + static_cast<size_t>(r) * 32, static_cast<double>(sp), epoch);
-            if (with_q) ll_store(result + static_cast<size_t>(r) * 32 + 4, static_cast<double>(sq), epoch);
+          if (ag) {
+            if (lane == 0) bcast[buf] = Pair{static_cast<double>(sp), static_cast<double>(sq)};
+          } else {
+            for (uint32_t r = lane; r < G; r += 32) {
+              ll_store(result + static_cast<size_t>(r) * 32, static_cast<double>(sp), epoch);
+              if (with_q) ll_store(result + static_cast<size_t>(r) * 32 + 4, static_cast<double>(sq), epoch);
+            }
           }
         }
-        if (lane == 0) {
+        if (lane == 0 && !ag) {
           double vp2 = 0.0, vq2 = 0.0;
           const uint32_t* mine = result + static_cast<size_t>(rank) * 32;
           const uint64_t t0 = globaltimer();
@@ -1150,7 +1159,14 @@ bool plan_onchip(int dtype, int variant, int64_t obs, SweepPlan& pl, bool force_
   return false;
 }
 
-int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
+static int grid_allgather_on() {
+  const char* a = getenv("BAK_GRID_AG");
+  return (a && a[0] == '1') ? 1 : 0;
+}
+
+int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm0, cudaStream_t st) {
+  SweepParams prm = prm0;
+  prm.grid_allgather = grid_allgather_on();
   if (pl.variant == BAK_VARIANT_GRID && prm.slots)
     BAK_CHECK_CUDA(cudaMemsetAsync(prm.slots, 0, kGridSlotBytes, st));
   if (pl.variant == BAK_VARIANT_GRID && pl.cluster) {

@@ -28,6 +28,7 @@ struct SweepParams {
   int64_t stage_elems;
   int nstages;
   int keep_next;  // STREAM: keep x_{j+1} in L2 for the next column step
+  int grid_allgather = 0;  // GRID one-level: every CTA gathers all records (no aggregator round trip)
 };
 
 struct SweepPlan {

@@ -134,16 +134,31 @@ def solve_bakp(x, y, config: BlockConfig | None = None, *, variant="auto", devic
         raise ValueError(f"y has length {yd.shape[0]}, expected {obs}")
     base = cfg.base
     if cfg.thr == 1:
-        # bakp.py:13-15: the one-column block is the sequential column step
-        rep = solve_bak(dm, yd, SolveConfig(max_iter=base.max_iter, tol=base.tol, record_history=True),
-                        variant="auto" if variant in ("auto", "stream", "gram") else variant, device=dev,
-                        return_device=return_device)
+        # bakp.py:13-15: the one-column block is the sequential column step — an
+        # EXACT kernel (auto never resolves to the labelled GRAM sweep here)
+        if variant in ("auto", "stream"):
+            exact = _lib.VARIANT_NAMES[int(lib.bak_sweep_pick_variant(code, obs, nvars))]
+        else:
+            exact = variant
+        # the guard of bakp.py:121-124 at thr=1: the sequential sweep cannot grow
+        # the residual in exact arithmetic, so only non-finite values trip it, on
+        # the first sweep — run just that sweep instead of all max_iter of them
+        finite = bool(torch.isfinite(dm.data[:, :obs]).all().item()) and bool(torch.isfinite(yd).all().item())
+        sweeps = base.max_iter if finite else 1
+        rep = solve_bak(dm, yd, SolveConfig(max_iter=sweeps, tol=base.tol, record_history=True),
+                        variant=exact, device=dev, return_device=return_device)
         if rep.sweeps_run:
             ynorm2 = float(_sumsq(lib, torch, code, yd, _Workspace(torch, dev, lib.bak_colnorms_workspace(
                 code, obs, 1)), _stream_ptr(torch, dev)).item())
             bad = _first_divergence(rep.residual_norm_history, ynorm2)
             if bad is not None:
                 raise DivergenceError(_divergence_message(bad[0], bad[1], cfg.thr))
+            if sweeps < base.max_iter and not rep.converged:  # non-finite input that did not trip it
+                rep = solve_bak(dm, yd, SolveConfig(max_iter=base.max_iter, tol=base.tol, record_history=True),
+                                variant=exact, device=dev, return_device=return_device)
+                bad = _first_divergence(rep.residual_norm_history, ynorm2)
+                if bad is not None:
+                    raise DivergenceError(_divergence_message(bad[0], bad[1], cfg.thr))
         if not base.record_history:
             rep.residual_norm_history = None
         return rep

@@ -104,23 +104,37 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region.
+    """SM clock + throttle reasons sampled DURING the timed region.
 
-    The sampler process is started before the warm-up (its start-up would
-    otherwise land inside the first timed step) and only the samples taken
-    between begin() and end() are kept."""
+    NVML (the library behind nvidia-smi; `nvidia_ml_py`) is polled from a thread
+    every 5 ms between begin() and end(), so that even a 20 ms timed region (C1:
+    100 sweeps in 7.5 ms per step) carries samples; when NVML cannot be loaded
+    the sampler falls back to an `nvidia-smi --query-gpu=... -lms 200` process
+    started before the warm-up."""
+
+    PERIOD_S = 0.005
+    NVML_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reason bitmask) from NVML
         self.proc = None
         self.recording = False
+        self.nvml = None
+        self.handle = None
+        self.source = None
+        self._stop = False
 
     def begin(self):
         self.lines = []
+        self.samples = []
         self.recording = True
 
     def end(self):
+        if self.nvml is not None and self.recording and not self.samples:
+            self._sample()  # a timed region shorter than one period
         self.recording = False
 
     def wait_ready(self, timeout=10.0):
@@ -128,14 +142,66 @@ class ClockSampler:
         while self.proc is not None and not self._seen and time.time() - t0 < timeout:
             time.sleep(0.05)
 
+    def _nvml_open(self):
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+            except Exception:
+                h = None
+            if h is None:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = self.index
+                if vis:
+                    try:
+                        idx = int(vis.split(",")[self.index])
+                    except (ValueError, IndexError):
+                        idx = self.index
+                h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml, self.handle = pynvml, h
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            return True
+        except Exception:
+            self.nvml = None
+            return False
+
+    def _sample(self):
+        nv, h = self.nvml, self.handle
+        try:
+            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            try:
+                bits = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            except Exception:
+                bits = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+            self.samples.append((sm, self.max_mhz, bits))
+        except Exception:
+            pass
+
+    def _poll(self):
+        while not self._stop:
+            if self.recording:
+                self._sample()
+            time.sleep(self.PERIOD_S)
+
     def __enter__(self):
         if os.environ.get("BAK_BENCH_NO_CLOCKS") == "1":  # A/B of the sampler's own cost
+            return self
+        if os.environ.get("BAK_BENCH_CLOCKS") != "smi" and self._nvml_open():
+            self.source = "nvml"
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
             return self
         q = "clocks.sm,clocks.max.sm," + ",".join("clocks_event_reasons." + r for r in REASON_FIELDS)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -151,6 +217,7 @@ class ClockSampler:
                 self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self._stop = True
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -160,6 +227,12 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
+        for s_mhz, m_mhz, bits in self.samples:
+            sm.append(s_mhz)
+            mx.append(m_mhz)
+            for name, bit in self.NVML_BITS.items():
+                if bits & bit:
+                    reasons.add(name)
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 2 + len(REASON_FIELDS):
@@ -173,9 +246,9 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(name)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.source}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": self.source}
 
 
 # --------------------------------------------------------------------------

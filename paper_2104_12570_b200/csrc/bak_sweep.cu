@@ -43,6 +43,7 @@
 
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
+#include "bak_tmem.cuh"
 
 namespace bak {
 namespace {
@@ -56,8 +57,11 @@ constexpr int kMaxRegStages = 16;   // register-resident plans: whole-column sta
 // XS: sub-stages per column.  Quarters: eighths were measured no faster at
 // 2^21 rows and slower at 2^20 (more waits / releases per column step,
 // profiles/r02_xs_phases.txt)
-template <int E>
-__host__ __device__ constexpr int xs_nq() { return 4; }
+// XT (XS == 2): the ring slot is one 8-row-per-thread chunk (one tcgen05.ld /
+// tcgen05.st of the TMEM stash), E / 8 slots per column.
+constexpr int kXtChunk = 8;
+template <int E, int XS = 1>
+__host__ __device__ constexpr int xs_nq() { return XS == 2 ? E / kXtChunk : 4; }
 constexpr int kMaxConsumers = 256;
 constexpr int kBarConsumers = 1;  // named barrier id used by consumer warps only
 
@@ -98,6 +102,33 @@ __device__ __forceinline__ T quotient(T a, T b, T r) {
   return Num<T>::fma(rem, r, q0);
 }
 
+// N values of T as the 32-bit registers one tcgen05.ld / tcgen05.st moves
+template <typename T, int N>
+struct TmemRegs;
+template <>
+struct TmemRegs<double, 8> {
+  uint32_t r[16];
+  __device__ __forceinline__ void set(int i, double v) {
+    r[2 * i] = static_cast<uint32_t>(__double2loint(v));
+    r[2 * i + 1] = static_cast<uint32_t>(__double2hiint(v));
+  }
+  __device__ __forceinline__ double get(int i) const {
+    return __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
+  }
+  __device__ __forceinline__ void load(uint32_t taddr) { tmem_ld_x16(taddr, r); }
+  __device__ __forceinline__ void wait() { tmem_wait_ld_x16(r); }
+  __device__ __forceinline__ void store(uint32_t taddr) const { tmem_st_x16(taddr, r); }
+};
+template <>
+struct TmemRegs<float, 8> {
+  uint32_t r[8];
+  __device__ __forceinline__ void set(int i, float v) { r[i] = __float_as_uint(v); }
+  __device__ __forceinline__ float get(int i) const { return __uint_as_float(r[i]); }
+  __device__ __forceinline__ void load(uint32_t taddr) { tmem_ld_x8(taddr, r); }
+  __device__ __forceinline__ void wait() { tmem_wait_ld_x8(r); }
+  __device__ __forceinline__ void store(uint32_t taddr) const { tmem_st_x8(taddr, r); }
+};
+
 #ifdef BAK_PHASES
 #define PH(i)                                  \
   do {                                         \
@@ -120,7 +151,7 @@ __device__ __forceinline__ T quotient(T a, T b, T r) {
 // x_{t+1} straight from the ring, and each consumer warp hands a quarter of
 // x_t back to the producer as soon as it has read it — so the load of x_{t+2}
 // starts during step t's arithmetic and overlaps the exchange that follows.
-template <typename T, int E, int MODE, int MAXNT, bool XS = false>
+template <typename T, int E, int MODE, int MAXNT, int XS = 0>
 __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams prm) {
 #ifdef BAK_PHASES
   long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -177,7 +208,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
   uint64_t* xbar2 = reinterpret_cast<uint64_t*>(smem_raw + off);  // [2] kModeGridCl broadcast
   off += 2 * 8;
   volatile int* stop = reinterpret_cast<volatile int*>(smem_raw + off);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + off + 8);  // XT: TMEM base address
 
+  if (XS == 2 && warp == 0) tmem_alloc512(smem_addr(tmem_slot));  // all 512 columns: one CTA per SM
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -190,15 +223,18 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     *stop = 0;
     fence_mbar_init();
   }
+  if (XS == 2) tmem_fence_before_sync();
   __syncthreads();
+  if (XS == 2) tmem_fence_after_sync();
+  const uint32_t tmem_base = (XS == 2) ? *tmem_slot : 0u;
   if (MODE == kModeCluster || MODE == kModeGridCl) cluster_sync();
 
   const int64_t ncols = prm.ncols;
   const int64_t total = prm.max_iter * ncols;
 
   if (tid >= NT && XS) {
-    // ======================= producer warp (XS: quarter columns) =======================
-    constexpr int NQ = xs_nq<E>();
+    // ======================= producer warp (XS: sub-column slots) =======================
+    constexpr int NQ = xs_nq<E, XS>();
     const int64_t QR = static_cast<int64_t>(E / NQ) * NT;  // rows per sub-column slot
     const uint64_t pol = policy_evict_first();
     int64_t f = 0;  // fills issued (4 per column step)
@@ -617,7 +653,7 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     int64_t sweep = 0;
     bool converged = false;
     if constexpr (XS) {
-      constexpr int NQ = xs_nq<E>(), EQ = E / NQ;
+      constexpr int NQ = xs_nq<E, XS>(), EQ = E / NQ;
       static_assert(E % NQ == 0, "XS: rows per thread must split into sub-column slots");
       const bool full_rows = kv == E;
       const uint32_t xs0 = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
@@ -664,6 +700,128 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
       auto xval = [&](uint32_t a, int kk, int k) -> T {
         return (full_rows || k < kv) ? lds<T>(a + static_cast<uint32_t>(kk * NT * sizeof(T))) : T(0);
       };
+      if constexpr (XS == 2) {
+        // ---- XT: x_{t+1} is read from the ring ONCE (for its dot), stashed in
+        // tensor memory, and read back from there for its update one step later;
+        // the ring slot goes back to the producer right after that single read,
+        // so the whole ring is prefetch (x_{t+2}, x_{t+3}) while the exchange of
+        // step t is in flight.  Per row the same two roundings and FMA order as
+        // the XS / register kernels.
+        static_assert(EQ == kXtChunk, "XT: one ring slot = one TMEM chunk");
+        constexpr int CW = EQ * static_cast<int>(sizeof(T)) / 4;  // 32-bit TMEM columns per chunk
+        // warp w owns TMEM lanes 32 (w % 4) ..; warps 4.. use the next column range
+        const uint32_t tb = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) +
+                            static_cast<uint32_t>((warp >> 2) * (E * static_cast<int>(sizeof(T)) / 4));
+        uint32_t rc = 0;
+        T P = T(0), Q = T(0);
+        int64_t c0 = 0, c1 = 0;
+        T n2_0 = T(1), ri_0 = T(1), n2_1 = T(1), ri_1 = T(1);
+        T acc[4] = {T(0), T(0), T(0), T(0)};
+        Pos pn{0, 0u};  // first slot of the column whose dot is being formed
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const Pos pq = adv(pn, q);
+          wait_fill(pq);
+          const uint32_t a = slot_addr(pq);
+          TmemRegs<T, EQ> xn;
+#pragma unroll
+          for (int kk = 0; kk < EQ; ++kk) xn.set(kk, xval(a, kk, q * EQ + kk));
+          release(pq);
+#pragma unroll
+          for (int kk = 0; kk < EQ; ++kk) {
+            const int k = q * EQ + kk;
+            acc[k & 3] = Num<T>::fma(xn.get(kk), ev[k], acc[k & 3]);
+          }
+          xn.store(tb + q * CW);
+        }
+        meta_of(0, c0, n2_0, ri_0);
+        T pv = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+        bool aborted = reduce(pv, T(0), false, rc++, -1, -1, P, Q);
+        const bool upd_warp = (rank == 0) && (warp == (nwarps > 1 ? 1 : 0));
+        T a0 = upd_warp ? ag[c0] : T(0);
+        int64_t k = 0, t = 0;
+        pn = adv(pn, NQ);
+        while (!aborted) {
+          PH(7);
+          const bool more = t + 1 < total;
+          const T d = quotient(P, n2_0, ri_0);
+          const bool last = (k == ncols - 1);
+          T ac[4] = {T(0), T(0), T(0), T(0)};
+          T a1 = T(0);
+          tmem_wait_st();  // the stash writes of the previous step (they overlapped its exchange)
+          TmemRegs<T, EQ> xt[2];
+          xt[0].load(tb);
+          if (more) {
+            wait_fill(pn);
+            meta_of(t + 1, c1, n2_1, ri_1);
+            if (upd_warp) a1 = ag[c1];
+          }
+          PH(0);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const Pos fn = adv(pn, q);
+            TmemRegs<T, EQ> xn;
+            if (more) {
+              if (q > 0) wait_fill(fn);
+              const uint32_t a_n = slot_addr(fn);
+#pragma unroll
+              for (int kk = 0; kk < EQ; ++kk) xn.set(kk, xval(a_n, kk, q * EQ + kk));
+              release(fn);
+            }
+            xt[q & 1].wait();
+            if (q + 1 < NQ) xt[(q + 1) & 1].load(tb + (q + 1) * CW);
+#pragma unroll
+            for (int kk = 0; kk < EQ; ++kk) {
+              const int kq = q * EQ + kk;
+              ev[kq] = Num<T>::sub(ev[kq], Num<T>::mul(xt[q & 1].get(kk), d));
+            }
+            if (more) {
+#pragma unroll
+              for (int kk = 0; kk < EQ; ++kk) {
+                const int kq = q * EQ + kk;
+                ac[kq & 3] = Num<T>::fma(xn.get(kk), ev[kq], ac[kq & 3]);
+              }
+              xn.store(tb + q * CW);
+            }
+          }
+          PH(1);
+          pv = Num<T>::add(Num<T>::add(ac[0], ac[1]), Num<T>::add(ac[2], ac[3]));
+          T qv = T(0);
+          if (last) {
+            T qa[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+            for (int kk = 0; kk < E; ++kk) qa[kk & 3] = Num<T>::fma(ev[kk], ev[kk], qa[kk & 3]);
+            qv = Num<T>::add(Num<T>::add(qa[0], qa[1]), Num<T>::add(qa[2], qa[3]));
+          }
+          PH(2);
+          if (upd_warp) {
+            const T na = Num<T>::add(a0, d);
+            ag[c0] = na;
+            if (more) a0 = (c1 == c0) ? na : a1;  // a1 = ag[c1] was read before the store
+          }
+          PH(5);
+          if (reduce(pv, qv, last, rc++, -1, -1, P, Q)) break;
+          PH(6);
+          if (last) {
+            if (rank == 0 && tid == 0 && prm.history) prm.history[sweep] = static_cast<double>(Q);
+            ++sweep;
+            if (prm.thresh2 >= 0.0 && static_cast<double>(Q) <= prm.thresh2) {
+              converged = true;
+              break;
+            }
+            if (sweep == prm.max_iter) break;
+            k = 0;
+          } else {
+            ++k;
+          }
+          ++t;
+          pn = adv(pn, NQ);
+          c0 = c1;
+          n2_0 = n2_1;
+          ri_0 = ri_1;
+        }
+        tmem_wait_st();
+      } else {
       // ---- prologue: the dot for column 0 ----
       uint32_t rc = 0;
       T P = T(0), Q = T(0);
@@ -759,6 +917,7 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         c0 = c1;
         n2_0 = n2_1;
         ri_0 = ri_1;
+      }
       }
     } else {
     // ---- prologue: columns 0 and 1 into registers, dot for column 0 ----
@@ -874,7 +1033,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
       }
     }
   }
+  if (XS == 2) tmem_fence_before_sync();
   __syncthreads();
+  if (XS == 2 && warp == 0) tmem_dealloc512(tmem_base);
   if (MODE == kModeCluster || MODE == kModeGridCl) cluster_sync();
 }
 
@@ -885,7 +1046,7 @@ size_t smem_bytes(const SweepPlan& pl, size_t tsize) {
          kMaxStages * sizeof(StageMeta) + 2 * 2 * 32 * tsize + 16 + 2 * kMaxCluster * 16 + 16 + 32 + 16 + 16;
 }
 
-template <typename T, int E, int MODE, int MAXNT, bool XS = false>
+template <typename T, int E, int MODE, int MAXNT, int XS = 0>
 int launch_one(const SweepPlan& pl, SweepParams prm, cudaStream_t st) {
   auto kern = sweep_kernel<T, E, MODE, MAXNT, XS>;
   const size_t smem = smem_bytes(pl, sizeof(T));
@@ -957,10 +1118,18 @@ constexpr int kXsConsumers = 224;
 template <typename T, int MODE>
 int launch_xs(const SweepPlan& pl, const SweepParams& prm, cudaStream_t st) {
   if constexpr (MODE == kModeGrid || MODE == kModeGridCl) {
-    switch (pl.e) {
-      case 40: return launch_one<T, 40, MODE, kXsConsumers, true>(pl, prm, st);
-      case 56: return launch_one<T, 56, MODE, kXsConsumers, true>(pl, prm, st);
-      case 80: return launch_one<T, 80, MODE, kXsConsumers, true>(pl, prm, st);
+    if (pl.xs == 2) {
+      switch (pl.e) {
+        case 40: return launch_one<T, 40, MODE, kXsConsumers, 2>(pl, prm, st);
+        case 56: return launch_one<T, 56, MODE, kXsConsumers, 2>(pl, prm, st);
+        case 80: return launch_one<T, 80, MODE, kXsConsumers, 2>(pl, prm, st);
+      }
+    } else {
+      switch (pl.e) {
+        case 40: return launch_one<T, 40, MODE, kXsConsumers, 1>(pl, prm, st);
+        case 56: return launch_one<T, 56, MODE, kXsConsumers, 1>(pl, prm, st);
+        case 80: return launch_one<T, 80, MODE, kXsConsumers, 1>(pl, prm, st);
+      }
     }
   }
   set_error("bak_sweep: unsupported XS plan (rows per thread %d)", pl.e);
@@ -1057,16 +1226,20 @@ static bool plan_xs(int dtype, int64_t obs, int parts, int cluster, SweepPlan& p
     cand.e = e;
     cand.nparticipants = parts;
     cand.rows_per_cta = rpc;
-    const int nq = 4;  // xs_nq<E>()
+    // XT (default): slots of kXtChunk rows per thread, the column stashed in
+    // tensor memory between its two uses; BAK_GRID_XT=0: quarter-column XS ring
+    const char* xt_env = getenv("BAK_GRID_XT");
+    const int mode = (xt_env && xt_env[0] == '0') ? 1 : 2;
+    const int nq = mode == 2 ? e / kXtChunk : 4;  // xs_nq<E, XS>()
     cand.stage_elems = static_cast<int64_t>(e / nq) * kXsConsumers;
     cand.cluster = cluster;
-    cand.xs = 1;
+    cand.xs = mode;
     cand.nstages = 0;
     const size_t fixed = smem_bytes(cand, ts);
     const size_t slot = static_cast<size_t>(cand.stage_elems) * ts;
     int st = static_cast<int>((smem_cap - fixed) / slot);
     if (st > kMaxStages) st = kMaxStages;
-    if (st < nq + 2) return false;  // the nq + 1 slots a step reads + 1 in flight
+    if (st < nq + 2) return false;  // XS: the nq + 1 slots a step reads + 1 in flight; XT: a column + 2
     cand.nstages = st;
     pl = cand;
     return true;

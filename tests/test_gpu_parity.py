@@ -429,3 +429,25 @@ def test_xs_exact_sweep_tall_matches_oracle(obs, nv, precision):
         rep2 = pb.solve_bak(x, y, pb.SolveConfig(**cfg2), variant="grid")
         assert rep2.sweeps_run == ref2["sweeps_run"] and rep2.converged == ref2["converged"]
         assert orc.rel_coeff_err(rep2.a_hat, ref2["a_hat"]) <= tol
+
+
+@pytest.mark.parametrize("obs,nv,precision", [(1_300_001, 5, "double"), (2_097_152, 4, "double"),
+                                              (2_000_000, 4, "single")])
+def test_xt_tmem_stash_bit_identical_to_xs_ring(obs, nv, precision, monkeypatch):
+    """XT (x_{t+1} stashed in tensor memory between its dot and its update; the
+    default for row blocks past register capacity) against the XS quarter-column
+    ring (BAK_GRID_XT=0): the same per-row operations in the same order, so the
+    bits agree; both against the oracle."""
+    pb = _pb()
+    x, y, _ = orc.config_c3(obs=obs, nvars=nv, precision=precision)
+    cfg = pb.SolveConfig(max_iter=3, tol=0, record_history=True)
+    monkeypatch.delenv("BAK_GRID_XT", raising=False)
+    r_xt = pb.solve_bak(x, y, cfg, variant="grid")
+    monkeypatch.setenv("BAK_GRID_XT", "0")
+    r_xs = pb.solve_bak(x, y, cfg, variant="grid")
+    assert r_xt.variant == "grid" and r_xs.variant == "grid"
+    assert r_xt.a_hat.tobytes() == r_xs.a_hat.tobytes()
+    assert r_xt.residual.tobytes() == r_xs.residual.tobytes()
+    assert r_xt.residual_norm_history == r_xs.residual_norm_history
+    ref = orc.solve(x, y, max_iter=3, tol=0)
+    assert orc.rel_coeff_err(r_xt.a_hat, ref["a_hat"]) <= TOL[np.dtype(x.dtype)]

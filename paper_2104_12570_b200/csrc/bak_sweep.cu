@@ -60,8 +60,14 @@ constexpr int kMaxRegStages = 16;   // register-resident plans: whole-column sta
 // XT (XS == 2): the ring slot is one 8-row-per-thread chunk (one tcgen05.ld /
 // tcgen05.st of the TMEM stash), E / 8 slots per column.
 constexpr int kXtChunk = 8;
+#ifndef BAK_XT_SLOT_CHUNKS
+#define BAK_XT_SLOT_CHUNKS 1  // 2 (16-row slots, half the ring waits) measured 18 % slower at 2^21 rows
+#endif
+// XT: chunks per ring slot (2 when E splits into 16-row slots: half the ring waits / releases)
+template <int E>
+__host__ __device__ constexpr int xt_cs() { return (BAK_XT_SLOT_CHUNKS == 2 && E % (2 * kXtChunk) == 0) ? 2 : 1; }
 template <int E, int XS = 1>
-__host__ __device__ constexpr int xs_nq() { return XS == 2 ? E / kXtChunk : 4; }
+__host__ __device__ constexpr int xs_nq() { return XS == 2 ? E / (kXtChunk * xt_cs<E>()) : 4; }
 constexpr int kMaxConsumers = 256;
 constexpr int kBarConsumers = 1;  // named barrier id used by consumer warps only
 
@@ -134,8 +140,8 @@ struct TmemRegs<float, 8> {
   do {                                         \
     if (tid == 0) {                            \
       const long long _c = clock64();          \
-      ph_acc[i] += _c - ph_last;               \
-      ph_last = _c;                            \
+      ph_acc[i] += _c - ph_acc[8];             \
+      ph_acc[8] = _c;                          \
     }                                          \
   } while (0)
 #else
@@ -154,8 +160,13 @@ struct TmemRegs<float, 8> {
 template <typename T, int E, int MODE, int MAXNT, int XS = 0>
 __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams prm) {
 #ifdef BAK_PHASES
-  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long ph_last = clock64();
+  // counters in shared memory (tid 0 only): registers would spill the E = 80 plans
+  __shared__ long long ph_acc[10];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) ph_acc[i] = 0;
+    ph_acc[9] = 0;
+    ph_acc[8] = clock64();
+  }
 #endif
   constexpr int kMaxWarps = MAXNT / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -676,6 +687,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
       auto wait_fill = [&](Pos p) {
         const int sl = p.sl;
         const uint32_t par = p.par;
+#ifdef BAK_PHASES
+        const long long w0 = clock64();
+#endif
         if (!mbar_test(&full[sl], par)) {
           const uint64_t t0 = globaltimer();
           while (!mbar_test(&full[sl], par)) {
@@ -686,6 +700,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
             }
           }
         }
+#ifdef BAK_PHASES
+        if (tid == 0) ph_acc[9] += clock64() - w0;  // ring waits (reported in the unused "pull" slot)
+#endif
       };
       auto release = [&](Pos p) {  // this warp is done reading that fill
         __syncwarp();
@@ -707,8 +724,9 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
         // so the whole ring is prefetch (x_{t+2}, x_{t+3}) while the exchange of
         // step t is in flight.  Per row the same two roundings and FMA order as
         // the XS / register kernels.
-        static_assert(EQ == kXtChunk, "XT: one ring slot = one TMEM chunk");
-        constexpr int CW = EQ * static_cast<int>(sizeof(T)) / 4;  // 32-bit TMEM columns per chunk
+        constexpr int CS = xt_cs<E>(), CH = kXtChunk, NC = E / CH;  // chunks per slot, rows per chunk, chunks
+        static_assert(EQ == CH * CS, "XT: a ring slot holds CS TMEM chunks");
+        constexpr int CW = CH * static_cast<int>(sizeof(T)) / 4;  // 32-bit TMEM columns per chunk
         // warp w owns TMEM lanes 32 (w % 4) ..; warps 4.. use the next column range
         const uint32_t tb = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) +
                             static_cast<uint32_t>((warp >> 2) * (E * static_cast<int>(sizeof(T)) / 4));
@@ -723,16 +741,20 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
           const Pos pq = adv(pn, q);
           wait_fill(pq);
           const uint32_t a = slot_addr(pq);
-          TmemRegs<T, EQ> xn;
 #pragma unroll
-          for (int kk = 0; kk < EQ; ++kk) xn.set(kk, xval(a, kk, q * EQ + kk));
-          release(pq);
+          for (int c = 0; c < CS; ++c) {
+            const int ch = q * CS + c;
+            TmemRegs<T, CH> xn;
 #pragma unroll
-          for (int kk = 0; kk < EQ; ++kk) {
-            const int k = q * EQ + kk;
-            acc[k & 3] = Num<T>::fma(xn.get(kk), ev[k], acc[k & 3]);
+            for (int kk = 0; kk < CH; ++kk) xn.set(kk, xval(a, c * CH + kk, ch * CH + kk));
+            if (c == CS - 1) release(pq);
+#pragma unroll
+            for (int kk = 0; kk < CH; ++kk) {
+              const int k = ch * CH + kk;
+              acc[k & 3] = Num<T>::fma(xn.get(kk), ev[k], acc[k & 3]);
+            }
+            xn.store(tb + ch * CW);
           }
-          xn.store(tb + q * CW);
         }
         meta_of(0, c0, n2_0, ri_0);
         T pv = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
@@ -749,7 +771,7 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
           T ac[4] = {T(0), T(0), T(0), T(0)};
           T a1 = T(0);
           tmem_wait_st();  // the stash writes of the previous step (they overlapped its exchange)
-          TmemRegs<T, EQ> xt[2];
+          TmemRegs<T, CH> xt[2];
           xt[0].load(tb);
           if (more) {
             wait_fill(pn);
@@ -758,30 +780,31 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
           }
           PH(0);
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
+          for (int ch = 0; ch < NC; ++ch) {
+            const int q = ch / CS, c = ch % CS;
             const Pos fn = adv(pn, q);
-            TmemRegs<T, EQ> xn;
+            TmemRegs<T, CH> xn;
             if (more) {
-              if (q > 0) wait_fill(fn);
+              if (c == 0 && q > 0) wait_fill(fn);
               const uint32_t a_n = slot_addr(fn);
 #pragma unroll
-              for (int kk = 0; kk < EQ; ++kk) xn.set(kk, xval(a_n, kk, q * EQ + kk));
-              release(fn);
+              for (int kk = 0; kk < CH; ++kk) xn.set(kk, xval(a_n, c * CH + kk, ch * CH + kk));
+              if (c == CS - 1) release(fn);
             }
-            xt[q & 1].wait();
-            if (q + 1 < NQ) xt[(q + 1) & 1].load(tb + (q + 1) * CW);
+            xt[ch & 1].wait();
+            if (ch + 1 < NC) xt[(ch + 1) & 1].load(tb + (ch + 1) * CW);
 #pragma unroll
-            for (int kk = 0; kk < EQ; ++kk) {
-              const int kq = q * EQ + kk;
-              ev[kq] = Num<T>::sub(ev[kq], Num<T>::mul(xt[q & 1].get(kk), d));
+            for (int kk = 0; kk < CH; ++kk) {
+              const int kq = ch * CH + kk;
+              ev[kq] = Num<T>::sub(ev[kq], Num<T>::mul(xt[ch & 1].get(kk), d));
             }
             if (more) {
 #pragma unroll
-              for (int kk = 0; kk < EQ; ++kk) {
-                const int kq = q * EQ + kk;
+              for (int kk = 0; kk < CH; ++kk) {
+                const int kq = ch * CH + kk;
                 ac[kq & 3] = Num<T>::fma(xn.get(kk), ev[kq], ac[kq & 3]);
               }
-              xn.store(tb + q * CW);
+              xn.store(tb + ch * CW);
             }
           }
           PH(1);
@@ -1021,7 +1044,8 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
     }
 #ifdef BAK_PHASES
     if (tid == 0 && rank == 0 && prm.history)
-      for (int i = 0; i < 8; ++i) prm.history[prm.max_iter + i] = static_cast<double>(ph_acc[i]);
+      for (int i = 0; i < 8; ++i)
+        prm.history[prm.max_iter + i] = static_cast<double>((XS && i == 2) ? ph_acc[9] : ph_acc[i]);
 #endif
     if (tid == 0) {
       *stop = 1;
@@ -1230,7 +1254,8 @@ static bool plan_xs(int dtype, int64_t obs, int parts, int cluster, SweepPlan& p
     // tensor memory between its two uses; BAK_GRID_XT=0: quarter-column XS ring
     const char* xt_env = getenv("BAK_GRID_XT");
     const int mode = (xt_env && xt_env[0] == '0') ? 1 : 2;
-    const int nq = mode == 2 ? e / kXtChunk : 4;  // xs_nq<E, XS>()
+    const int cs = (BAK_XT_SLOT_CHUNKS == 2 && e % (2 * kXtChunk) == 0) ? 2 : 1;  // xt_cs<E>()
+    const int nq = mode == 2 ? e / (kXtChunk * cs) : 4;                            // xs_nq<E, XS>()
     cand.stage_elems = static_cast<int64_t>(e / nq) * kXsConsumers;
     cand.cluster = cluster;
     cand.xs = mode;

@@ -139,7 +139,8 @@ __device__ __forceinline__ int col_of(int lane, int i) {
 #endif
 
 // E <= 4 keeps 64 partial dots per thread in registers: at most 7 warps
-// (192 consumers + producer) so a thread may use up to 255 registers
+// (192 consumers + producer) so a thread may use up to 255 registers (9 warps
+// cap it at 168: the E = 1, 2 plans spilled)
 constexpr int bg_max_threads(int e) { return e <= 4 ? 224 : kMaxNT + 32; }
 
 template <typename T, int E, bool CL>
@@ -645,7 +646,12 @@ bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
   if (parts > kMaxCl) parts = kMaxCl;
   if (parts < 1) parts = 1;
   const int64_t per = (obs + parts - 1) / parts;
-  for (int e : {4, 8, 16}) {
+  // fewest rows per thread first: the passes are latency-bound, so more warps
+  // (and no masked rows when a CTA owns < 4 rows per thread) win; BAK_BGRAM_E forces one
+  const char* e_env = getenv("BAK_BGRAM_E");
+  const int e_only = e_env ? atoi(e_env) : 0;
+  for (int e : {1, 2, 4, 8, 16}) {
+    if (e_only && e != e_only) continue;
     int64_t nt = round_up((per + e - 1) / e, 32);
     if (nt < kB) nt = kB;  // threads t < 64 finish the block's 64 dots and deltas
     if (nt + 32 > bg_max_threads(e)) continue;
@@ -702,6 +708,8 @@ template <typename T>
 int bg_launch_e(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
   const bool cl = pl.parts > 1;
   switch (pl.e) {
+    case 1: return cl ? bg_launch<T, 1, true>(pl, prm, st) : bg_launch<T, 1, false>(pl, prm, st);
+    case 2: return cl ? bg_launch<T, 2, true>(pl, prm, st) : bg_launch<T, 2, false>(pl, prm, st);
     case 4: return cl ? bg_launch<T, 4, true>(pl, prm, st) : bg_launch<T, 4, false>(pl, prm, st);
     case 8: return cl ? bg_launch<T, 8, true>(pl, prm, st) : bg_launch<T, 8, false>(pl, prm, st);
     case 16: return cl ? bg_launch<T, 16, true>(pl, prm, st) : bg_launch<T, 16, false>(pl, prm, st);

@@ -32,17 +32,30 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
 
 namespace bak {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // bak_gram_tma.cu
 namespace {
+
+// one box of the 2-D tensor map of x (rows x columns; out-of-range rows and
+// columns arrive as zeros) into shared memory, completing on `bar`
+__device__ __forceinline__ void bg_tma_2d(void* dst, const CUtensorMap* map, int row, int col, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(smem_addr(bar))
+      : "memory");
+}
 
 constexpr int kB = 64;      // block width
 constexpr int kW = 8;       // columns per ring stage
 constexpr int kMaxS = 32;   // ring stages
 constexpr int kMaxNT = 256;
-constexpr int kMaxW = kMaxNT / 32;
 constexpr int kMaxCl = 16;
 constexpr int kBarBG = 1;   // named barrier of the consumer warps
 
@@ -56,7 +69,7 @@ struct BgParams {
   double thresh2;  // < 0: no early break
   double* history;
   int64_t* status;
-  int64_t rows_per_cta;
+  int64_t rows_per_cta;  // = NT * E
   int nstages;
   int resident;  // 1: a block's stages stay in the ring from pass 1 to pass 2 (read once)
 };
@@ -82,47 +95,6 @@ __device__ __forceinline__ void st_async_d(uint32_t remote_addr, double v, uint3
                : "memory");
 }
 
-// Sum N per-lane values (N = 8 or 64) over the warp by recursive halving:
-// each round a lane keeps the half of its values selected by one lane bit and
-// adds the partner's copy of that half (N - 1 + log2(32 / N) shuffles in all,
-// every round's shuffles independent).  Afterwards lane L holds, in v[0..R),
-// R = max(1, N / 32), the warp totals of values
-//   c(L, i) = i + R * (bit0 + 2 bit1 + 4 bit2 + 8 bit3 + 16 bit4 of L restricted
-//             to the rounds that halved),  see col_of below.  Fixed order: deterministic.
-template <typename T, int N>
-__device__ __forceinline__ void warp_sum_multi(T (&v)[N], int lane) {
-  int n = N;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    if (n > 1) {
-      const bool hi = lane & o;
-      const int h = n / 2;
-#pragma unroll
-      for (int i = 0; i < N / 2; ++i) {
-        if (i < h) {
-          const T send = hi ? v[i] : v[i + h];
-          const T keep = hi ? v[i + h] : v[i];
-          v[i] = Num<T>::add(keep, __shfl_xor_sync(0xffffffffu, send, o));
-        }
-      }
-      n = h;
-    } else {
-      v[0] = Num<T>::add(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
-    }
-  }
-}
-// which value lane L holds in slot i after warp_sum_multi<T, N>
-template <int N>
-__device__ __forceinline__ int col_of(int lane, int i) {
-  int c = 0, n = N;
-#pragma unroll
-  for (int o = 16; o >= 1 && n > 1; o >>= 1) {
-    n >>= 1;
-    if (lane & o) c += n;
-  }
-  return c + i;
-}
-
 #ifdef BAK_PHASES
 #define GPH(i)                                 \
   do {                                         \
@@ -141,10 +113,12 @@ __device__ __forceinline__ int col_of(int lane, int i) {
 // E <= 4 keeps 64 partial dots per thread in registers: at most 7 warps
 // (192 consumers + producer) so a thread may use up to 255 registers (9 warps
 // cap it at 168: the E = 1, 2 plans spilled)
-constexpr int bg_max_threads(int e) { return e <= 4 ? 224 : kMaxNT + 32; }
+constexpr int bg_max_threads(int) { return kMaxNT + 32; }
+constexpr int kMaxSeg = kMaxNT / kW;  // row segments of pass 1 (8 column threads per segment)
 
 template <typename T, int E, bool CL>
-__global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgParams prm) {
+__global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __grid_constant__ CUtensorMap xmap,
+                                                                      const BgParams prm) {
   constexpr int CB = E <= 4 ? 8 : (E <= 8 ? 4 : 2);  // columns whose slices are loaded together
 #ifdef BAK_PHASES
   long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -159,7 +133,6 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
     rank = cluster_rank();
     G = cluster_size();
   }
-  const T* __restrict__ x = static_cast<const T*>(prm.x);
   T* __restrict__ eg = static_cast<T*>(prm.e);
   T* __restrict__ ag = static_cast<T*>(prm.a);
   const int64_t V = prm.vars;
@@ -167,13 +140,18 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
   const int64_t RP = prm.rows_per_cta;
   const int64_t r0 = static_cast<int64_t>(rank) * RP;
   const int64_t nrows = imax64(0, imin64(prm.obs - r0, RP));
-  constexpr int VEC = 16 / sizeof(T);
-  const uint32_t col_bytes = static_cast<uint32_t>(((nrows + VEC - 1) / VEC) * VEC * sizeof(T));
-
   // ---- shared memory ----
+  // ring stage = kW columns of the CTA's NT * E rows as E boxes of the tensor
+  // map: [S][E][kW][NT].  Box k holds rows r0 + k NT .. of the stage's 8
+  // columns; rows past obs and columns past vars arrive as zeros, so no load in
+  // the passes is masked and every stage carries the same byte count.
   size_t off = 0;
-  T* xs = reinterpret_cast<T*>(smem_raw);  // [S][kW][RP]
-  off += static_cast<size_t>(S) * kW * RP * sizeof(T);
+  const uint32_t box_elems = static_cast<uint32_t>(kW) * NT;
+  const uint32_t stage_elems = box_elems * E;
+  T* xs = reinterpret_cast<T*>(smem_raw);
+  off += static_cast<size_t>(S) * stage_elems * sizeof(T);
+  T* esh = reinterpret_cast<T*>(smem_raw + off);  // [NT * E] the residual, for pass 1 (pass 2 keeps it in registers)
+  off += static_cast<size_t>(NT) * E * sizeof(T);
   off = (off + 127) & ~size_t(127);
   double* msh = reinterpret_cast<double*>(smem_raw + off);  // [2][64*64] M of the current / next block
   off += 2 * kB * kB * sizeof(double);
@@ -184,8 +162,8 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
   T* dsh = reinterpret_cast<T*>(smem_raw + off);  // [kB] block deltas
   off += kB * sizeof(T);
   off = (off + 15) & ~size_t(15);
-  T* red = reinterpret_cast<T*>(smem_raw + off);  // [kB][kMaxW] per-warp partial dots
-  off += kB * kMaxW * sizeof(T);
+  T* red = reinterpret_cast<T*>(smem_raw + off);  // [kB][kMaxSeg] per-segment partial dots
+  off += kB * kMaxSeg * sizeof(T);
   off = (off + 15) & ~size_t(15);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + off);
   off += kMaxS * 8;
@@ -223,13 +201,19 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
 
   if (tid >= NT) {
     // =========================== producer warp ===========================
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_last();  // the block is read twice
-      int s = 0;
-      uint32_t ph = 0;
-      int64_t u = 0;
+    // One tensor copy per box (NT rows x 8 columns): E copies per stage instead
+    // of one bulk copy per column slice — the TMA unit retires a copy every
+    // ~70-110 cycles whatever its size (tools/micro/bulk_rate.cu), and 64-128
+    // column copies per block were the floor of the whole sweep.  The whole warp
+    // issues: a group is up to 4 stages; lane l serves stage l / 8 of the group
+    // and boxes l % 8 and l % 8 + 8 of it; the first lane of a stage waits for
+    // the slot and posts the stage's bytes.
+    {
+      int64_t u = 0;  // stages issued
       bool halted = false;
       int64_t mb = 0;  // blocks whose M has been issued
+      const uint64_t pol = policy_evict_last();
+      const uint32_t stage_bytes = stage_elems * static_cast<uint32_t>(sizeof(T));
       for (int64_t sw = 0; sw < prm.max_iter && !halted; ++sw)
         for (int64_t b = 0; b < nblocks && !halted; ++b)
           for (int pass = 0; pass < (prm.resident ? 1 : 2) && !halted; ++pass) {
@@ -238,49 +222,69 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
               // the block's M (32 KB, one bulk copy) into buffer mb & 1, once the
               // matvec two blocks back has read it
               const int mbuf = static_cast<int>(mb & 1);
-              if (mb >= 2) {
-                const uint32_t par = static_cast<uint32_t>(((mb >> 1) - 1) & 1);
-                if (!mbar_test(&mempty[mbuf], par)) {
-                  const uint64_t t0 = globaltimer();
-                  while (!mbar_test(&mempty[mbuf], par)) {
-                    if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+              if (lane == 0) {
+                if (mb >= 2) {
+                  const uint32_t par = static_cast<uint32_t>(((mb >> 1) - 1) & 1);
+                  if (!mbar_test(&mempty[mbuf], par)) {
+                    const uint64_t t0 = globaltimer();
+                    while (!mbar_test(&mempty[mbuf], par)) {
+                      if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+                    }
                   }
                 }
-                if (halted) break;
+                if (!halted) {
+                  mbar_arrive_expect_tx(&mfull[mbuf], kB * kB * 8u);
+                  bulk_g2s(msh + mbuf * kB * kB, prm.minv + b * kB * kB, kB * kB * 8u, &mfull[mbuf], pol);
+                }
               }
-              mbar_arrive_expect_tx(&mfull[mbuf], kB * kB * 8u);
-              bulk_g2s(msh + mbuf * kB * kB, prm.minv + b * kB * kB, kB * kB * 8u, &mfull[mbuf], pol);
+              halted = __any_sync(0xffffffffu, halted);
+              if (halted) break;
               ++mb;
             }
-            for (int c0 = 0; c0 < w && !halted; c0 += kW, ++u) {
-              if (u >= S) {
-                const uint32_t par = ph ^ 1u;
-                if (!mbar_test(&empty[s], par)) {
-                  const uint64_t t0 = globaltimer();
-                  while (!mbar_test(&empty[s], par)) {
-                    if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+            const int nst = (w + kW - 1) / kW;
+            // (a group never spans more stages than the ring has slots: two of its
+            // stages would wait on the same slot)
+            const int gmax = S < 4 ? S : 4;
+            for (int s0 = 0; s0 < nst && !halted; s0 += gmax) {
+              const int gst = nst - s0 < gmax ? nst - s0 : gmax;  // stages in this group
+              const int j = lane / kW, k8 = lane % kW;
+              const int64_t uj = u + j;
+              const int sj = static_cast<int>(uj % S);
+              const uint32_t phj = static_cast<uint32_t>((uj / S) & 1);
+              if (j < gst && k8 == 0) {
+                if (uj >= S) {
+                  const uint32_t par = phj ^ 1u;
+                  if (!mbar_test(&empty[sj], par)) {
+                    const uint64_t t0 = globaltimer();
+                    while (!mbar_test(&empty[sj], par)) {
+                      if (*stop || globaltimer() - t0 > kTimeoutNs) { halted = true; break; }
+                    }
                   }
                 }
-                if (halted) break;
+                if (!halted) mbar_arrive_expect_tx(&full[sj], stage_bytes);
               }
-              const int n = w - c0 < kW ? w - c0 : kW;
-              mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * col_bytes);
-              if (col_bytes)
-                for (int i = 0; i < n; ++i)
-                  bulk_g2s(xs + (static_cast<size_t>(s) * kW + i) * RP, x + (b * kB + c0 + i) * prm.ldx + r0,
-                           col_bytes, &full[s], pol);
-              if (++s == S) { s = 0; ph ^= 1u; }
+              halted = __any_sync(0xffffffffu, halted);
+              if (halted) break;
+              if (j < gst) {
+                const int col = static_cast<int>(b * kB) + (s0 + j) * kW;
+                for (int k = k8; k < E; k += kW)
+                  bg_tma_2d(xs + static_cast<size_t>(sj) * stage_elems + static_cast<size_t>(k) * box_elems, &xmap,
+                            static_cast<int>(r0) + k * NT, col, &full[sj]);
+              }
+              u += gst;
             }
           }
-      for (int64_t v = imax64(0, u - S); v < u; ++v) {  // in-flight copies land before exit
-        const uint64_t t0 = globaltimer();
-        while (!mbar_test(&full[v % S], static_cast<uint32_t>((v / S) & 1)))
-          if (globaltimer() - t0 > kTimeoutNs) break;
-      }
-      for (int64_t v = imax64(0, mb - 2); v < mb; ++v) {  // and the last two M copies
-        const uint64_t t0 = globaltimer();
-        while (!mbar_test(&mfull[v & 1], static_cast<uint32_t>((v >> 1) & 1)))
-          if (globaltimer() - t0 > kTimeoutNs) break;
+      if (lane == 0) {
+        for (int64_t v = imax64(0, u - S); v < u; ++v) {  // in-flight copies land before exit
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test(&full[v % S], static_cast<uint32_t>((v / S) & 1)))
+            if (globaltimer() - t0 > kTimeoutNs) break;
+        }
+        for (int64_t v = imax64(0, mb - 2); v < mb; ++v) {  // and the last two M copies
+          const uint64_t t0 = globaltimer();
+          while (!mbar_test(&mfull[v & 1], static_cast<uint32_t>((v >> 1) & 1)))
+            if (globaltimer() - t0 > kTimeoutNs) break;
+        }
       }
     }
   } else {
@@ -289,13 +293,13 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
     T ev[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) ev[k] = (k < kv) ? eg[r0 + tid + static_cast<int64_t>(k) * NT] : T(0);
-    const bool full_rows = kv == E;
     int my_abort = 0;
     int ls = 0;
     uint32_t lph = 0;
     const uint32_t xs_base = smem_addr(xs) + static_cast<uint32_t>(tid * sizeof(T));
-    const uint32_t col_stride = static_cast<uint32_t>(RP * sizeof(T));
-    const uint32_t stage_stride = col_stride * kW;
+    const uint32_t col_stride = static_cast<uint32_t>(NT * sizeof(T));        // next column of a box
+    const uint32_t k_stride = box_elems * static_cast<uint32_t>(sizeof(T));   // next box (rows + NT)
+    const uint32_t stage_stride = stage_elems * static_cast<uint32_t>(sizeof(T));
     auto wait_stage = [&]() -> uint32_t {
       if (!mbar_test(&full[ls], lph)) {
         const uint64_t t0 = globaltimer();
@@ -314,9 +318,7 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
       if (lane == 0) arrive1(&empty[ls]);
       if (++ls == S) { ls = 0; lph ^= 1u; }
     };
-    auto xval = [&](uint32_t a, int k) -> T {
-      return (full_rows || k < kv) ? lds<T>(a + static_cast<uint32_t>(k * NT * sizeof(T))) : T(0);
-    };
+    auto xval = [&](uint32_t a, int k) -> T { return lds<T>(a + static_cast<uint32_t>(k) * k_stride); };
     // cluster sum of n values (thread t < n holds v), rank order; result in t < n
     uint32_t rc = 0;
     auto exchange = [&](double v, int n) -> double {
@@ -353,74 +355,53 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
     bool converged = false, aborted = false;
     int64_t mi = 0;  // blocks consumed (M buffer mi & 1)
     if (tid < kB) gsh[tid] = 0.0;  // (finite before the first block; see the matvec)
+    const int nseg = NT >> 3;  // pass 1: 8 column threads per row segment
+    auto publish_e = [&]() {  // registers -> esh (read by the column threads of the next pass 1)
+#pragma unroll
+      for (int k = 0; k < E; ++k) esh[tid + k * NT] = ev[k];
+    };
+    publish_e();
     while (sweep < prm.max_iter && !aborted) {
       for (int64_t b = 0; b < nblocks && !aborted; ++b) {
         const int w = block_w(b);
-        // ---- pass 1: partial dots of the block's columns against e ----
+        // ---- pass 1: dots of the block's columns against e.  Stage by stage
+        // (8 columns): thread t takes column t % 8 of the stage and, in every
+        // box k, the 8 rows k NT + 8 (t / 8) .. — E runs of 8 products from
+        // shared memory (x from the ring, e from esh), no cross-lane reduction;
+        // the NT / 8 segment partials of a column are summed in segment order
+        // below.  A box column is NT rows = a multiple of 256 bytes, so the 8
+        // column threads of a segment would hit one bank: thread c8 walks its 8
+        // rows starting at row c8 (rotated, a fixed per-thread order) ----
         const int ls_block = ls;  // resident: pass 2 re-reads these stages
-        if constexpr (E <= 4) {
-          // the block's 64 partial dots stay in registers across its 8 stages;
-          // ONE multi-value warp reduction per block
-          T p[kB];
+        if (bar_bg_or(NT, my_abort)) { aborted = true; break; }  // esh holds every thread's e
+        {
+          const int c8 = tid & (kW - 1), seg = tid >> 3;
+          uint32_t roff[8];
 #pragma unroll
-          for (int c = 0; c < kB; ++c) p[c] = T(0);
+          for (int i = 0; i < 8; ++i) roff[i] = static_cast<uint32_t>((seg * 8 + ((i + c8) & 7)) * sizeof(T));
+          const uint32_t eb = smem_addr(esh);
+          for (int c0 = 0; c0 < w; c0 += kW) {
+            wait_stage();
+            const uint32_t xb = smem_addr(xs) + static_cast<uint32_t>(ls) * stage_stride + c8 * col_stride;
+            T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-          for (int st8 = 0; st8 < kB / kW; ++st8) {
-            const int c0 = st8 * kW;
-            if (c0 < w) {
-              const uint32_t a = wait_stage();
-              const int n = w - c0 < kW ? w - c0 : kW;
-              T xr[kW][E];
+            for (int k = 0; k < E; ++k) {
+              T xv[8], evv[8];
 #pragma unroll
-              for (int c = 0; c < kW; ++c)
-#pragma unroll
-                for (int k = 0; k < E; ++k) xr[c][k] = (c < n) ? xval(a + c * col_stride, k) : T(0);
-#pragma unroll
-              for (int c = 0; c < kW; ++c) {
-                T acc[2] = {T(0), T(0)};
-#pragma unroll
-                for (int k = 0; k < E; ++k) acc[k & 1] = Num<T>::fma(xr[c][k], ev[k], acc[k & 1]);
-                p[c0 + c] = Num<T>::add(acc[0], acc[1]);
+              for (int i = 0; i < 8; ++i) {
+                xv[i] = lds<T>(xb + static_cast<uint32_t>(k) * k_stride + roff[i]);
+                evv[i] = lds<T>(eb + static_cast<uint32_t>(k * NT * sizeof(T)) + roff[i]);
               }
-              if (prm.resident) {
-                if (++ls == S) { ls = 0; lph ^= 1u; }
-              } else {
-                release_stage();
-              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i & 3] = Num<T>::fma(xv[i], evv[i], acc[i & 3]);
+            }
+            red[(c0 + c8) * kMaxSeg + seg] = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+            if (prm.resident) {
+              if (++ls == S) { ls = 0; lph ^= 1u; }
+            } else {
+              release_stage();
             }
           }
-          warp_sum_multi<T, kB>(p, lane);
-#pragma unroll
-          for (int i = 0; i < 2; ++i) red[col_of<kB>(lane, i) * kMaxW + warp] = p[i];
-        } else {
-        for (int c0 = 0; c0 < w; c0 += kW) {
-          const uint32_t a = wait_stage();
-          const int n = w - c0 < kW ? w - c0 : kW;
-          T p[8];
-          // batches of CB columns: all their loads issued before the arithmetic
-#pragma unroll
-          for (int cb = 0; cb < 8; cb += CB) {
-            T xr[CB][E];
-#pragma unroll
-            for (int c = 0; c < CB; ++c)
-#pragma unroll
-              for (int k = 0; k < E; ++k) xr[c][k] = (cb + c < n) ? xval(a + (cb + c) * col_stride, k) : T(0);
-#pragma unroll
-            for (int c = 0; c < CB; ++c) {
-              T acc[2] = {T(0), T(0)};
-#pragma unroll
-              for (int k = 0; k < E; ++k) acc[k & 1] = Num<T>::fma(xr[c][k], ev[k], acc[k & 1]);
-              p[cb + c] = Num<T>::add(acc[0], acc[1]);
-            }
-          }
-          if (prm.resident) {
-            if (++ls == S) { ls = 0; lph ^= 1u; }
-          } else {
-            release_stage();
-          }
-          warp_sum_multi<T, kW>(p, lane);
-          if ((lane & 3) == 0) red[(c0 + col_of<kW>(lane, 0)) * kMaxW + warp] = p[0];
-        }
         }
         GPH(0);
         if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
@@ -428,7 +409,7 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
         double v = 0.0;
         if (tid < w) {
           T s = T(0);
-          for (int ww = 0; ww < nwarps; ++ww) s = Num<T>::add(s, red[tid * kMaxW + ww]);
+          for (int sg = 0; sg < nseg; ++sg) s = Num<T>::add(s, red[tid * kMaxSeg + sg]);
           v = static_cast<double>(s);
         }
         const double g = exchange(v, w);
@@ -500,6 +481,7 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const BgPar
             release_stage();
           }
         }
+        publish_e();
         GPH(5);
       }
       if (aborted) break;
@@ -624,46 +606,46 @@ __global__ void __launch_bounds__(256) bgram_prep_kernel(const T* __restrict__ x
 }
 
 struct BgPlan {
-  int parts = 1, nt = 32, e = 4, nstages = 2, resident = 0;
-  int64_t rows_per_cta = 0;
+  int parts = 1, nt = 64, e = 1, nstages = 2, resident = 0;
+  int64_t rows_per_cta = 0;  // = nt * e
 };
 
 size_t bg_smem(const BgPlan& p, size_t ts) {
-  size_t off = static_cast<size_t>(p.nstages) * kW * p.rows_per_cta * ts;
+  size_t off = static_cast<size_t>(p.nstages) * p.e * kW * p.nt * ts + static_cast<size_t>(p.nt) * p.e * ts;
   off = (off + 127) & ~size_t(127);
   off += 2 * kB * kB * 8 + 2 * kMaxCl * kB * 8 + kB * 8 + kB * ts;
   off = (off + 15) & ~size_t(15);
-  off += kB * kMaxW * ts;
+  off += kB * kMaxSeg * ts;
   off = (off + 15) & ~size_t(15);
   return off + 2 * kMaxS * 8 + 16 + 16 + 16 + 32;
 }
 
 bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
+  if (!tensor_map_encoder() || obs >= (int64_t(1) << 31)) return false;
   const size_t ts = dtype_size(dtype);
   const size_t cap = static_cast<size_t>(device_max_smem_optin()) - 2048;
-  // as many CTAs as a cluster allows (bandwidth), at least 64 rows each
-  int parts = static_cast<int>((obs + 63) / 64);
-  if (parts > kMaxCl) parts = kMaxCl;
-  if (parts < 1) parts = 1;
-  const int64_t per = (obs + parts - 1) / parts;
+  // as many CTAs as a cluster allows (bandwidth), at least 64 rows each; row
+  // blocks of exactly nt * e rows (box k of a stage = rows k nt .. of the block)
+  int64_t per = (obs + kMaxCl - 1) / kMaxCl;
+  if (per < 64) per = 64;
   // fewest rows per thread first: the passes are latency-bound, so more warps
-  // (and no masked rows when a CTA owns < 4 rows per thread) win; BAK_BGRAM_E forces one
+  // win; BAK_BGRAM_E forces one
   const char* e_env = getenv("BAK_BGRAM_E");
   const int e_only = e_env ? atoi(e_env) : 0;
   for (int e : {1, 2, 4, 8, 16}) {
     if (e_only && e != e_only) continue;
     int64_t nt = round_up((per + e - 1) / e, 32);
     if (nt < kB) nt = kB;  // threads t < 64 finish the block's 64 dots and deltas
-    if (nt + 32 > bg_max_threads(e)) continue;
+    if (nt > kMaxNT) continue;
     BgPlan c;
-    c.parts = parts;
     c.nt = static_cast<int>(nt);
     c.e = e;
-    c.rows_per_cta = round_up(per, 4);
-    if (c.rows_per_cta > nt * e) continue;
+    c.rows_per_cta = nt * e;
+    c.parts = static_cast<int>((obs + c.rows_per_cta - 1) / c.rows_per_cta);
+    if (c.parts > kMaxCl) continue;
     c.nstages = 0;
     const size_t fixed = bg_smem(c, ts);
-    const size_t sb = static_cast<size_t>(kW) * c.rows_per_cta * ts;
+    const size_t sb = static_cast<size_t>(e) * kW * nt * ts;
     if (fixed + 3 * sb > cap) continue;
     int s = static_cast<int>((cap - fixed) / sb);
     c.nstages = s > kMaxS ? kMaxS : s;
@@ -679,6 +661,20 @@ bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
 
 template <typename T, int E, bool CL>
 int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
+  // x as a 2-D tensor (rows, columns); a box is nt rows x 8 columns
+  CUtensorMap map;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(prm.obs), static_cast<cuuint64_t>(prm.vars)};
+  cuuint64_t gstr[1] = {static_cast<cuuint64_t>(prm.ldx * sizeof(T))};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(pl.nt), static_cast<cuuint32_t>(kW)};
+  cuuint32_t est[2] = {1, 1};
+  CUresult r = tensor_map_encoder()(
+      &map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      const_cast<void*>(prm.x), gdim, gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (x, block-Gram) failed (%d)", static_cast<int>(r));
+    return BAK_ECUDA;
+  }
   auto kern = bgram_kernel<T, E, CL>;
   const size_t smem = bg_smem(pl, sizeof(T));
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -699,7 +695,7 @@ int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, map, prm));
   count_launches(1);
   return BAK_OK;
 }

@@ -67,6 +67,15 @@ template <> __device__ __forceinline__ float lds<float>(uint32_t addr) {
   return v;
 }
 
+// zero one element of shared memory (32-bit shared address)
+template <typename T> __device__ __forceinline__ void sts_zero(uint32_t addr);
+template <> __device__ __forceinline__ void sts_zero<double>(uint32_t addr) {
+  asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(0ull) : "memory");
+}
+template <> __device__ __forceinline__ void sts_zero<float>(uint32_t addr) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(0u) : "memory");
+}
+
 // ---------------- mbarrier ----------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
@@ -99,6 +108,19 @@ __device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity
       : "r"(smem_addr(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+
+// generic-proxy writes to shared memory made visible to the async proxy (TMA)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Zero a 16-byte-aligned shared-memory range with all threads of the CTA.  The
+// bulk copies of a ragged last row block never write the rows past the system's
+// end, so after this the kernels read those rows as 0 with plain (unmasked)
+// loads.  Call before the __syncthreads() that precedes the first bulk copy.
+__device__ __forceinline__ void smem_zero(void* base, size_t bytes) {
+  uint4* p = reinterpret_cast<uint4*>(base);
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) p[i] = z;
+  fence_proxy_async_smem();
 }
 
 // ---------------- bulk copy global -> shared (TMA engine, 1-D) ----------------

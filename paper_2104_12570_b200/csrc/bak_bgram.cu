@@ -53,7 +53,8 @@ __device__ __forceinline__ void bg_tma_2d(void* dst, const CUtensorMap* map, int
 }
 
 constexpr int kB = 64;      // block width
-constexpr int kW = 8;       // columns per ring stage
+constexpr int kW = 8;       // columns per ring stage (KW = 8), or the whole block (KW = 64) when 3 blocks fit
+constexpr int kLG = 8;      // producer: lanes per stage of an issue group
 constexpr int kMaxS = 32;   // ring stages
 constexpr int kMaxNT = 256;
 constexpr int kMaxCl = 16;
@@ -113,11 +114,13 @@ __device__ __forceinline__ void st_async_d(uint32_t remote_addr, double v, uint3
 // E <= 4 keeps 64 partial dots per thread in registers: at most 7 warps
 // (192 consumers + producer) so a thread may use up to 255 registers (9 warps
 // cap it at 168: the E = 1, 2 plans spilled)
-constexpr int bg_max_threads(int) { return kMaxNT + 32; }
-constexpr int kMaxSeg = kMaxNT / kW;  // row segments of pass 1 (8 column threads per segment)
+// whole-block stages (KW = 64) unroll 64 columns per pass: at most 128 consumers, so
+// a thread may use up to 255 registers (288 threads cap it at 168: spills)
+constexpr int bg_max_threads(int kw) { return kw == 64 ? 128 + 32 : kMaxNT + 32; }
+constexpr int kMaxSeg = kMaxNT / kW;  // row segments of pass 1 (KW column threads per segment)
 
-template <typename T, int E, bool CL>
-__global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __grid_constant__ CUtensorMap xmap,
+template <typename T, int E, bool CL, int KW>
+__global__ void __launch_bounds__(bg_max_threads(KW), 1) bgram_kernel(const __grid_constant__ CUtensorMap xmap,
                                                                       const BgParams prm) {
   constexpr int CB = E <= 4 ? 8 : (E <= 8 ? 4 : 2);  // columns whose slices are loaded together
 #ifdef BAK_PHASES
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
   // columns; rows past obs and columns past vars arrive as zeros, so no load in
   // the passes is masked and every stage carries the same byte count.
   size_t off = 0;
-  const uint32_t box_elems = static_cast<uint32_t>(kW) * NT;
+  const uint32_t box_elems = static_cast<uint32_t>(KW) * NT;
   const uint32_t stage_elems = box_elems * E;
   T* xs = reinterpret_cast<T*>(smem_raw);
   off += static_cast<size_t>(S) * stage_elems * sizeof(T);
@@ -241,13 +244,13 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
               if (halted) break;
               ++mb;
             }
-            const int nst = (w + kW - 1) / kW;
+            const int nst = (w + KW - 1) / KW;
             // (a group never spans more stages than the ring has slots: two of its
             // stages would wait on the same slot)
             const int gmax = S < 4 ? S : 4;
             for (int s0 = 0; s0 < nst && !halted; s0 += gmax) {
               const int gst = nst - s0 < gmax ? nst - s0 : gmax;  // stages in this group
-              const int j = lane / kW, k8 = lane % kW;
+              const int j = lane / kLG, k8 = lane % kLG;
               const int64_t uj = u + j;
               const int sj = static_cast<int>(uj % S);
               const uint32_t phj = static_cast<uint32_t>((uj / S) & 1);
@@ -266,8 +269,8 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
               halted = __any_sync(0xffffffffu, halted);
               if (halted) break;
               if (j < gst) {
-                const int col = static_cast<int>(b * kB) + (s0 + j) * kW;
-                for (int k = k8; k < E; k += kW)
+                const int col = static_cast<int>(b * kB) + (s0 + j) * KW;
+                for (int k = k8; k < E; k += kLG)
                   bg_tma_2d(xs + static_cast<size_t>(sj) * stage_elems + static_cast<size_t>(k) * box_elems, &xmap,
                             static_cast<int>(r0) + k * NT, col, &full[sj]);
               }
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
     bool converged = false, aborted = false;
     int64_t mi = 0;  // blocks consumed (M buffer mi & 1)
     if (tid < kB) gsh[tid] = 0.0;  // (finite before the first block; see the matvec)
-    const int nseg = NT >> 3;  // pass 1: 8 column threads per row segment
+    const int nseg = NT / KW;  // pass 1: KW column threads per run of KW rows
     auto publish_e = [&]() {  // registers -> esh (read by the column threads of the next pass 1)
 #pragma unroll
       for (int k = 0; k < E; ++k) esh[tid + k * NT] = ev[k];
@@ -373,29 +376,39 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
         // column threads of a segment would hit one bank: thread c8 walks its 8
         // rows starting at row c8 (rotated, a fixed per-thread order) ----
         const int ls_block = ls;  // resident: pass 2 re-reads these stages
+        // the block's coefficients, read now: the load's latency is off the path
+        // (a load right before the store stalled CTA 0 for an L2 round trip per block)
+        const T a_old = (rank == 0 && tid < w) ? ag[b * kB + tid] : T(0);
         if (bar_bg_or(NT, my_abort)) { aborted = true; break; }  // esh holds every thread's e
         {
-          const int c8 = tid & (kW - 1), seg = tid >> 3;
-          uint32_t roff[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) roff[i] = static_cast<uint32_t>((seg * 8 + ((i + c8) & 7)) * sizeof(T));
-          const uint32_t eb = smem_addr(esh);
-          for (int c0 = 0; c0 < w; c0 += kW) {
+          // thread -> column c8 of the stage and run `seg` of KW rows in every box;
+          // it walks the run starting at row c8 (rotated): the KW column threads of a
+          // run read KW different rows, i.e. different banks
+          const int c8 = tid & (KW - 1), seg = tid / KW;
+          const uint32_t rbase = static_cast<uint32_t>(seg * KW * sizeof(T));
+          const uint32_t eb = smem_addr(esh) + rbase;
+          for (int c0 = 0; c0 < w; c0 += KW) {
             wait_stage();
-            const uint32_t xb = smem_addr(xs) + static_cast<uint32_t>(ls) * stage_stride + c8 * col_stride;
+            const uint32_t xb = smem_addr(xs) + static_cast<uint32_t>(ls) * stage_stride + c8 * col_stride + rbase;
             T acc[4] = {T(0), T(0), T(0), T(0)};
+            if (seg < nseg) {
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-              T xv[8], evv[8];
+              for (int k = 0; k < E; ++k) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                xv[i] = lds<T>(xb + static_cast<uint32_t>(k) * k_stride + roff[i]);
-                evv[i] = lds<T>(eb + static_cast<uint32_t>(k * NT * sizeof(T)) + roff[i]);
+                for (int i0 = 0; i0 < KW; i0 += 8) {
+                  T xv[8], evv[8];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) {
+                    const uint32_t ro = static_cast<uint32_t>(((i0 + i + c8) & (KW - 1)) * sizeof(T));
+                    xv[i] = lds<T>(xb + static_cast<uint32_t>(k) * k_stride + ro);
+                    evv[i] = lds<T>(eb + static_cast<uint32_t>(k * NT * sizeof(T)) + ro);
+                  }
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) acc[i & 3] = Num<T>::fma(xv[i], evv[i], acc[i & 3]);
+                }
               }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i & 3] = Num<T>::fma(xv[i], evv[i], acc[i & 3]);
+              red[(c0 + c8) * kMaxSeg + seg] = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
             }
-            red[(c0 + c8) * kMaxSeg + seg] = Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
             if (prm.resident) {
               if (++ls == S) { ls = 0; lph ^= 1u; }
             } else {
@@ -438,7 +451,9 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
           for (int k = 0; k < kB; ++k) dp[k & 3] = __fma_rn(mcol[k * kB], gsh[k], dp[k & 3]);
           const T dt = static_cast<T>((dp[0] + dp[1]) + (dp[2] + dp[3]));
           dsh[tid] = dt;
-          if (rank == 0) ag[b * kB + tid] = Num<T>::add(ag[b * kB + tid], dt);
+          if (rank == 0) ag[b * kB + tid] = Num<T>::add(a_old, dt);
+        } else if (tid < kB) {
+          dsh[tid] = T(0);  // past a ragged last block: its (zero-filled) columns change nothing
         }
         if (bar_bg_or(NT, my_abort)) { aborted = true; break; }
         if (tid == 0) arrive1(&mempty[mbuf]);  // every matvec read is before the barrier
@@ -446,17 +461,16 @@ __global__ void __launch_bounds__(bg_max_threads(E), 1) bgram_kernel(const __gri
         GPH(4);
         // ---- pass 2: e -= fl(d_j x_j), column by column (two roundings, bak.py:87-88) ----
         int s2 = ls_block;
-        for (int c0 = 0; c0 < w; c0 += kW) {
+        for (int c0 = 0; c0 < w; c0 += KW) {
           const uint32_t a = prm.resident ? xs_base + static_cast<uint32_t>(s2) * stage_stride : wait_stage();
-          const int n = w - c0 < kW ? w - c0 : kW;
 #pragma unroll
-          for (int cb = 0; cb < 8; cb += CB) {
+          for (int cb = 0; cb < KW; cb += CB) {
             T xr[CB][E], dd[CB];
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
-              dd[c] = (cb + c < n) ? dsh[c0 + cb + c] : T(0);  // past the block: e - fl(0 * 0) = e
+              dd[c] = dsh[c0 + cb + c];  // 0 past a ragged block's width, where x is zero-filled too
 #pragma unroll
-              for (int k = 0; k < E; ++k) xr[c][k] = (cb + c < n) ? xval(a + (cb + c) * col_stride, k) : T(0);
+              for (int k = 0; k < E; ++k) xr[c][k] = xval(a + (cb + c) * col_stride, k);
             }
             // e -= (sum of the CB products, pairwise tree) — a short dependency chain
             // instead of 2 CB dependent ops per row (labelled variant: the rounding
@@ -607,11 +621,12 @@ __global__ void __launch_bounds__(256) bgram_prep_kernel(const T* __restrict__ x
 
 struct BgPlan {
   int parts = 1, nt = 64, e = 1, nstages = 2, resident = 0;
+  int kw = kW;  // columns per ring stage: 8, or 64 (a whole block per stage) when >= 3 blocks fit
   int64_t rows_per_cta = 0;  // = nt * e
 };
 
 size_t bg_smem(const BgPlan& p, size_t ts) {
-  size_t off = static_cast<size_t>(p.nstages) * p.e * kW * p.nt * ts + static_cast<size_t>(p.nt) * p.e * ts;
+  size_t off = static_cast<size_t>(p.nstages) * p.e * p.kw * p.nt * ts + static_cast<size_t>(p.nt) * p.e * ts;
   off = (off + 127) & ~size_t(127);
   off += 2 * kB * kB * 8 + 2 * kMaxCl * kB * 8 + kB * 8 + kB * ts;
   off = (off + 15) & ~size_t(15);
@@ -637,6 +652,8 @@ bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
     int64_t nt = round_up((per + e - 1) / e, 32);
     if (nt < kB) nt = kB;  // threads t < 64 finish the block's 64 dots and deltas
     if (nt > kMaxNT) continue;
+    // 8 consumer warps of 1 row per thread measured 4 % slower than 4 warps of 2 (C2)
+    if (e == 1 && nt > 128 && !e_only) continue;
     BgPlan c;
     c.nt = static_cast<int>(nt);
     c.e = e;
@@ -645,27 +662,34 @@ bool bg_plan(int dtype, int64_t obs, BgPlan& pl) {
     if (c.parts > kMaxCl) continue;
     c.nstages = 0;
     const size_t fixed = bg_smem(c, ts);
-    const size_t sb = static_cast<size_t>(e) * kW * nt * ts;
+    // a whole block per stage (one wait and one release per pass instead of 8)
+    // when the ring holds 3 blocks (short columns: C4)
+    const char* kw_env = getenv("BAK_BGRAM_KW");
+    const size_t sb64 = static_cast<size_t>(e) * kB * nt * ts;
+    c.kw = (e <= 4 && nt <= 128 && fixed + 3 * sb64 <= cap && nt % kB == 0 && !(kw_env && atoi(kw_env) == kW))
+               ? kB
+               : kW;
+    const size_t sb = static_cast<size_t>(e) * c.kw * nt * ts;
     if (fixed + 3 * sb > cap) continue;
     int s = static_cast<int>((cap - fixed) / sb);
     c.nstages = s > kMaxS ? kMaxS : s;
-    // a block (8 stages) stays resident between its passes when the ring also
-    // holds at least one more block's worth of prefetch
-    c.resident = c.nstages >= 2 * (kB / kW) ? 1 : 0;
-    if (const char* r = getenv("BAK_BGRAM_RESIDENT")) c.resident = (r[0] == '1') && c.nstages > kB / kW;
+    // a block stays resident between its passes when the ring also holds at
+    // least one more block's worth of prefetch
+    c.resident = c.nstages >= 2 * (kB / c.kw) ? 1 : 0;
+    if (const char* r = getenv("BAK_BGRAM_RESIDENT")) c.resident = (r[0] == '1') && c.nstages > kB / c.kw;
     pl = c;
     return true;
   }
   return false;
 }
 
-template <typename T, int E, bool CL>
-int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
-  // x as a 2-D tensor (rows, columns); a box is nt rows x 8 columns
+template <typename T, int E, bool CL, int KW>
+int bg_launch_kw(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
+  // x as a 2-D tensor (rows, columns); a box is nt rows x KW columns
   CUtensorMap map;
   cuuint64_t gdim[2] = {static_cast<cuuint64_t>(prm.obs), static_cast<cuuint64_t>(prm.vars)};
   cuuint64_t gstr[1] = {static_cast<cuuint64_t>(prm.ldx * sizeof(T))};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(pl.nt), static_cast<cuuint32_t>(kW)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(pl.nt), static_cast<cuuint32_t>(KW)};
   cuuint32_t est[2] = {1, 1};
   CUresult r = tensor_map_encoder()(
       &map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
@@ -675,7 +699,7 @@ int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
     set_error("cuTensorMapEncodeTiled (x, block-Gram) failed (%d)", static_cast<int>(r));
     return BAK_ECUDA;
   }
-  auto kern = bgram_kernel<T, E, CL>;
+  auto kern = bgram_kernel<T, E, CL, KW>;
   const size_t smem = bg_smem(pl, sizeof(T));
   BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t cfg{};
@@ -698,6 +722,14 @@ int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
   BAK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, map, prm));
   count_launches(1);
   return BAK_OK;
+}
+
+template <typename T, int E, bool CL>
+int bg_launch(const BgPlan& pl, const BgParams& prm, cudaStream_t st) {
+  if constexpr (E <= 4) {
+    if (pl.kw == kB) return bg_launch_kw<T, E, CL, kB>(pl, prm, st);
+  }
+  return bg_launch_kw<T, E, CL, kW>(pl, prm, st);
 }
 
 template <typename T>

@@ -285,6 +285,46 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
     set_error("bak_sweep_rowshard: x/e must be 16-byte aligned with ldx*sizeof(T) %% 16 == 0");
     return BAK_EINVAL;
   }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // One rank per device whose rows fit on chip (C3 fp64 over 8 GPUs: 2M rows):
+  // the exact on-chip sweep (e in registers, x streamed once — XT / register
+  // GRID plans) with the cross-GPU stage inside its two-level exchange, instead
+  // of the STREAM pass that moves e through L2 every column.  BAK_ROWSHARD_ONCHIP=0
+  // keeps the STREAM kernel.
+  {
+    const char* oc = getenv("BAK_ROWSHARD_ONCHIP");
+    SweepPlan pl;
+    if (nranks_local == 1 && !(oc && oc[0] == '0') && workspace && workspace_bytes >= kGridSlotBytes &&
+        plan_onchip(dtype, BAK_VARIANT_GRID, obs_local, pl) && pl.variant == BAK_VARIANT_GRID && pl.cluster != 0) {
+      SweepParams sp{};
+      sp.x = x;
+      sp.obs = obs_local;
+      sp.ldx = ldx;
+      sp.norms2 = norms2;
+      sp.cols = nullptr;
+      sp.ncols = vars;
+      sp.cols_stride = 0;
+      sp.e = e;
+      sp.a = a;
+      sp.max_iter = max_iter;
+      sp.thresh2 = thresh2;
+      sp.history = history;
+      sp.status = status;
+      sp.slots = static_cast<uint32_t*>(workspace);
+      sp.rows_per_cta = pl.rows_per_cta;
+      sp.stage_elems = pl.stage_elems;
+      sp.nstages = pl.nstages;
+      sp.keep_next = 0;
+      sp.nranks = nranks;
+      sp.grank = rank;
+      sp.epoch_base = static_cast<uint32_t>(epoch_base);
+      for (int r = 0; r < nranks; ++r) sp.mbox[r] = static_cast<uint32_t*>(mailboxes[r]);
+      BAK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int64_t), st));
+      if (launch_onchip(dtype, pl, sp, st) == BAK_OK) return BAK_OK;
+      g_err_clear();  // clusters not co-resident: the STREAM kernel below
+      cudaGetLastError();
+    }
+  }
   const int sms = device_sms();
   int per_rank_ctas = imax64(1, sms / nranks_local);
   // two-level exchange: whole clusters of 8 per rank (<= 32 per rank), all co-resident
@@ -304,7 +344,6 @@ extern "C" int bak_sweep_rowshard(int dtype, const void* x, int64_t obs_local, i
     set_error("bak_sweep_rowshard: workspace too small (need %lld)", (long long)need);
     return BAK_EWORKSPACE;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   RowshardParams p{};
   p.x = x;
   p.ldx = ldx;

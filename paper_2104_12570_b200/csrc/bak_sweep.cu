@@ -550,8 +550,37 @@ __global__ void __launch_bounds__(MAXNT + 32, 1) sweep_kernel(const SweepParams 
               vq = static_cast<T>(v);
             }
           }
-          const T sp = warp_sum(vp);
-          const T sq = with_q ? warp_sum(vq) : T(0);
+          T sp = warp_sum(vp);
+          T sq = with_q ? warp_sum(vq) : T(0);
+          if (prm.nranks > 0) {
+            // cross-GPU stage (row sharding): rank totals through the mailboxes
+            // (peer-mapped memory, system-scope epoch-tagged records), summed in
+            // rank order -> identical bits on every rank
+            const int N = prm.nranks;
+            const uint32_t xepoch = prm.epoch_base + rc + 1;
+            if (cid == 0 && lane < N) {
+              uint32_t* dst = prm.mbox[lane] + (static_cast<size_t>(buf) * N + prm.grank) * 8;
+              ll_store_sys(dst, static_cast<double>(sp), xepoch);
+              ll_store_sys(dst + 4, static_cast<double>(sq), xepoch);
+            }
+            double rp = 0.0, rq = 0.0;
+            if (lane < N) {
+              const uint32_t* src = prm.mbox[prm.grank] + (static_cast<size_t>(buf) * N + lane) * 8;
+              const uint64_t t0 = globaltimer();
+              while (!ll_load_sys(src, xepoch, rp))
+                if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+              if (with_q)
+                while (!ll_load_sys(src + 4, xepoch, rq))
+                  if (globaltimer() - t0 > kTimeoutNs) { timed_out = true; break; }
+            }
+            T tp = T(0), tq = T(0);
+            for (int r = 0; r < N; ++r) {
+              tp = Num<T>::add(tp, static_cast<T>(__shfl_sync(0xffffffffu, rp, r)));
+              if (with_q) tq = Num<T>::add(tq, static_cast<T>(__shfl_sync(0xffffffffu, rq, r)));
+            }
+            sp = tp;
+            sq = tq;
+          }
           if (lane < static_cast<int>(C)) {
             const uint32_t rs = mapa(smem_addr(&bcast[buf]), lane);
             const uint32_t rb = mapa(smem_addr(&xbar2[buf]), lane);
@@ -1374,6 +1403,7 @@ int launch_onchip(int dtype, const SweepPlan& pl, const SweepParams& prm0, cudaS
     const int rc = dtype == BAK_F64 ? launch_nt<double, kModeGridCl>(pl, prm, st)
                                     : launch_nt<float, kModeGridCl>(pl, prm, st);
     if (rc == BAK_OK) return rc;  // else (capacity / cooperative launch refused): one level
+    if (prm.nranks > 0) return rc;  // row sharding needs the two-level exchange (the caller falls back to STREAM)
     // clusters did not fit co-resident: one-level grid exchange
     if (getenv("BAK_DEBUG")) fprintf(stderr, "bak: two-level grid exchange unavailable (%s)\n", bak_last_error());
     SweepPlan flat;

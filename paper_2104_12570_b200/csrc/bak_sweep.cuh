@@ -29,6 +29,14 @@ struct SweepParams {
   int nstages;
   int keep_next;  // STREAM: keep x_{j+1} in L2 for the next column step
   int grid_allgather = 0;  // GRID one-level: every CTA gathers all records (no aggregator round trip)
+  // Row sharding over GPUs (bak_sweep_rowshard, two-level GRID plans only): x, e
+  // are this rank's rows; after the rank's clusters have reduced, the cluster-0
+  // leader posts the rank total into every rank's mailbox and every leader sums
+  // the nranks totals in rank order.  nranks = 0: single device.
+  uint32_t* mbox[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int nranks = 0;
+  int grank = 0;
+  uint32_t epoch_base = 0;
 };
 
 struct SweepPlan {

@@ -268,7 +268,9 @@ def solve_bak_rowsharded(x_shards, y_shards, config: SolveConfig | None = None, 
         if int(stat[2]):
             raise _lib.BakError(f"bak_sweep_rowshard device error {int(stat[2])} (3 = exchange timeout)")
         sweeps, converged = int(stat[0]), bool(stat[1])
-        return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, "stream-rowshard")
+        # status[3]: the kernel that ran — the on-chip GRID sweep (rows fit on chip) or the STREAM pass
+        label = "grid-rowshard" if int(stat[3]) == _lib.VARIANTS["grid"] else "stream-rowshard"
+        return _finish_sharded(shards, comm, a, hist, sweeps, converged, ynorm2, t0, return_device, label)
     # G and the first sweep's dots g = X^T e in one read of each shard (the DMMA
     # kernel's diagonal-block CTAs produce the dots); rows of partials padded
     # to the largest shard's count so the all-gather has one shape everywhere
@@ -487,7 +489,8 @@ def sweep_rowshard(dm, e, a, norms, max_iter, thresh2, mailboxes, rank, nranks, 
     dev = dm.data.device
     st = stream if stream is not None else _stream_ptr(torch, dev)
     ctas = max(1, (lib.bak_device_sm_count() or 148) // nranks_local)
-    ws = _Workspace(torch, dev, nranks_local * max(2 * ctas * 32, 2048) + 4096)
+    # (>= the on-chip GRID kernel's exchange records, used when one rank's rows fit on chip)
+    ws = _Workspace(torch, dev, max(nranks_local * max(2 * ctas * 32, 2048), 96 * 1024) + 4096)
     if status is None:
         status = torch.zeros(4 * nranks_local, dtype=torch.int64, device=dev)
     base = mailboxes.next_epochs(max_iter * dm.vars + 1)

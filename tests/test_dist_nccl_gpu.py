@@ -32,7 +32,7 @@ def test_nccl_rowsharded_solves_match_oracle():
     res = json.loads(line[len("RESULT "):])
     assert res["gram"]["sweeps"] == 5 and res["gram"]["err"] <= 1e-10
     assert res["stream"]["sweeps"] == 5 and res["stream"]["err"] <= 1e-10
-    assert res["stream"]["label"] == "stream-rowshard"
+    assert res["stream"]["label"] in ("stream-rowshard", "grid-rowshard")  # on-chip sweep when the rows fit
     assert res["batched"]["nsys"] == 24 and res["batched"]["sweeps"] == 40 and res["batched"]["err"] <= 1e-4
 
 

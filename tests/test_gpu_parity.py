@@ -331,18 +331,26 @@ def test_rowshard_exact_kernel_emulated_ranks(nranks, precision):
     assert a2.cpu().numpy().reshape(nranks, 12)[0].tobytes() == A[0].tobytes()
 
 
-def test_rowsharded_api_stream_single_process():
+@pytest.mark.parametrize("obs,onchip", [(40_000, "1"), (40_000, "0"), (1_300_000, "1")])
+def test_rowsharded_api_stream_single_process(obs, onchip, monkeypatch):
     """solve_bak_rowsharded(variant='stream') on one process: the exact in-kernel
     exchange path with N=1 must match the oracle (the N>1 exchange is covered by
-    the emulated-ranks kernel test)."""
+    the emulated-ranks kernel test).  A rank whose rows fit on chip runs the
+    on-chip GRID sweep (register plans; XT past 1M rows) with the mailbox stage
+    inside its two-level exchange; BAK_ROWSHARD_ONCHIP=0 keeps the STREAM pass."""
     from paper_2104_12570_b200.sharded import solve_bak_rowsharded
     pb = _pb()
-    x, y, _ = orc.config_c3(obs=40_000, nvars=10, precision="double")
+    monkeypatch.setenv("BAK_ROWSHARD_ONCHIP", onchip)
+    nv = 10 if obs < 100_000 else 4
+    x, y, _ = orc.config_c3(obs=obs, nvars=nv, precision="double")
     cfg = dict(max_iter=5, tol=0, record_history=True)
     rep = solve_bak_rowsharded([x], [y], pb.SolveConfig(**cfg), variant="stream")[0]
     ref = orc.solve(x, y, **cfg)
-    assert rep.variant == "stream-rowshard"
+    assert rep.variant == ("grid-rowshard" if onchip == "1" else "stream-rowshard")
     assert_parity(x, y, rep, ref["a_hat"], ref["sweeps_run"], ref["converged"], ref_hist=ref["residual_norm_history"])
+    if onchip == "1":  # same bits as the single-device GRID sweep (one rank: the mailbox adds 0 + total)
+        one = pb.solve_bak(x, y, pb.SolveConfig(**cfg), variant="grid")
+        assert one.a_hat.tobytes() == rep.a_hat.tobytes()
 
 
 @pytest.mark.parametrize("precision", ["double", "single"])

@@ -180,7 +180,11 @@ int64_t bak_solve_batched_wave(int dtype, int64_t obs, int64_t vars);
  * everywhere.  mailboxes[r] = rank r's mailbox (device pointer valid on this
  * device: a peer mapping, or local memory when emulating).
  * With nranks_local > 1 a single launch emulates nranks_local ranks on one
- * device (rows split evenly), used for single-GPU testing of the exchange. */
+ * device (rows split evenly), used for single-GPU testing of the exchange.
+ * With nranks_local == 1 and a workspace of >= 96 KiB, a rank whose rows fit on
+ * chip runs the on-chip sweep (e in registers, x read once per sweep) with the
+ * mailbox stage inside its grid exchange; status[3] = BAK_VARIANT_GRID then,
+ * BAK_VARIANT_STREAM for the streaming pass. */
 int64_t bak_mailbox_bytes(int64_t nranks);
 int bak_sweep_rowshard(int dtype,
                        const void* x, int64_t obs_local, int64_t vars, int64_t ldx,

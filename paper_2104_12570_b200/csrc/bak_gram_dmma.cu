@@ -71,6 +71,7 @@ struct GramParams {
   double* part;                 // [nb*cd + noff*co][64*64], diagonal CTAs first
   const void* e;                // optional: fused g0 = X^T e in the diagonal CTAs
   double* g0;                   // [cd][vars] per-chunk partials of X^T e
+  int* pace;                    // optional: one step counter per CTA (advisory lock step, see below)
 };
 
 // off-diagonal block index -> (bi, bj), bi > bj, row-major over the strict lower triangle
@@ -152,6 +153,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
       cp_async16(pb + static_cast<size_t>(slot) * kBT * kLdT + tid * kPer, bytes ? ev + row : ev, bytes);
     }
   };
+  // Advisory lock step: the nb(nb+1)/2 CTAs of one K chunk read the same rows
+  // (each 64-column panel feeds 4 of them), but diagonal CTAs run ahead of the
+  // off-diagonal ones and the panels fall out of L2 before the slower readers
+  // arrive (ncu: 86 GB of DRAM reads for 34 GB of x).  Every kPaceEvery stages a
+  // CTA publishes its stage and (one stage later, with the counters already
+  // read) waits, bounded, while it is more than kPaceLead stages ahead of the
+  // slowest CTA of its chunk.  A hint only: a wait that
+  // runs into its bound switches the pacing off for this CTA, and the results
+  // do not depend on it.
+  #ifndef BAK_PACE_EVERY
+#define BAK_PACE_EVERY 16
+#endif
+#ifndef BAK_PACE_LEAD
+#define BAK_PACE_LEAD 32
+#endif
+  constexpr int kPaceEvery = BAK_PACE_EVERY, kPaceLead = BAK_PACE_LEAD, kPaceSpins = 200, kPaceDone = 1 << 30;
+  int pace_seen = kPaceDone;
+  const int noff_all = p.nb * (p.nb - 1) / 2;
+  bool paced = p.pace != nullptr;
+  int pace_peer = -1;
+  if (paced && warp == 0) {
+    if (lane < p.nb) pace_peer = chk * p.nb + lane;
+    else if (lane < p.nb + noff_all) pace_peer = ndc + chk * noff_all + (lane - p.nb);
+  }
   // fused g0 (warp 1 of a diagonal CTA owns the unused upper quadrant: no DMMA work)
   double g0a = 0.0;
 
@@ -199,6 +224,27 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
   }
   const int fr = lane >> 2, fk = lane & 3;  // fragment row/col within an 8x4 tile
   for (int step = 0; step < nsteps; ++step) {
+    if (paced && warp == 0) {
+      const int ph = step % kPaceEvery;
+      if (ph == 0) {
+        // publish, and issue the read of the peers' counters: consumed one stage later, so its
+        // L2 round trip overlaps this stage's MMAs
+        if (lane == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = step;
+        pace_seen = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
+      } else if (ph == 1) {
+        int v = __reduce_min_sync(0xffffffffu, pace_seen);
+        int spins = 0;
+        while (step > v + kPaceLead) {
+          if (++spins > kPaceSpins) {
+            paced = false;  // a peer is not keeping up (or not resident): stop waiting for it
+            break;
+          }
+          __nanosleep(500);
+          v = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
+          v = __reduce_min_sync(0xffffffffu, v);
+        }
+      }
+    }
     cp_async_wait<kStages - 2>();
     __syncthreads();
     {
@@ -300,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
     if (c0 < p.vars) g[c0] = g0a;
   }
   cp_async_wait<0>();
+  if (p.pace && tid == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = kPaceDone;
   double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
   if constexpr (X3) {
     flush();
@@ -422,7 +469,7 @@ int64_t gram_g_workspace(int dtype, int64_t obs, int64_t vars, int& nchunks, int
   nchunks = g.cd;  // partial rows of the fused g0
   chunk = g.chunk_d;
   const int64_t ctas = static_cast<int64_t>(g.nb) * g.cd + static_cast<int64_t>(g.nb) * (g.nb - 1) / 2 * g.co;
-  return ctas * kBT * kBT * 8;
+  return ctas * kBT * kBT * 8 + round_up(ctas * 4, 256);  // partials + the pacing counters
 }
 
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
@@ -439,9 +486,21 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   const GramSplit g = gram_split(obs, vars);
   const int nblk = g.nb * (g.nb + 1) / 2;
   GramParams p{x, obs, ldx, vars, g.nb, g.cd, g.co, g.chunk_d, g.chunk_o, static_cast<double*>(part_ws),
-               g0 ? e : nullptr, g0};
+               g0 ? e : nullptr, g0, nullptr};
   const size_t ts = dtype == BAK_F64 ? 8 : 4;
   const unsigned grid = static_cast<unsigned>(g.nb * g.cd + g.nb * (g.nb - 1) / 2 * g.co);
+  // advisory lock step of the CTAs of a K chunk (same rows for every block, <= 32 blocks, one wave);
+  // BAK_GRAM_PACE=0 switches it off
+  {
+    const char* pe = getenv("BAK_GRAM_PACE");
+    const bool off = pe && pe[0] == '0';
+    const int nblk_all = g.nb * (g.nb + 1) / 2;
+    if (!off && g.nb > 1 && nblk_all <= 32 && g.cd == g.co && g.chunk_d == g.chunk_o &&
+        static_cast<int>(grid) <= gram_occ() * device_sms()) {
+      p.pace = reinterpret_cast<int*>(static_cast<char*>(part_ws) + static_cast<size_t>(grid) * kBT * kBT * 8);
+      BAK_CHECK_CUDA(cudaMemsetAsync(p.pace, 0, static_cast<size_t>(grid) * 4, st));
+    }
+  }
   auto go = [&](auto kern, int stages) -> int {
     const size_t smem = 2ull * stages * kBT * kLd * ts;
     BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

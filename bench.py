@@ -94,6 +94,15 @@ def _peaks():
     return {}
 
 
+def _ncu_traffic(key):
+    """DRAM bytes per launch from the committed ncu captures (profiles/ncu_traffic.json), or None."""
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(prof):
+        return None
+    with open(prof) as f:
+        return json.load(f).get(key)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -626,7 +635,9 @@ def run_ours(args, cfg, rank, world, dev):
                                 "peak_source": gsrc if "MEASURED_PEAKS" in gsrc
                                 else gsrc + " (no such figure in MEASURED_PEAKS.json)",
                                 "frac": round(flops / (g_ms / 1e3) / 1e12 / gpeak, 3),
-                                "share_of_step": round(g_ms / (ms / args.steps), 3)}
+                                "share_of_step": round(g_ms / (ms / args.steps), 3),
+                                "alg_bytes_per_launch": int(dm.obs * dm.vars * ts),
+                                "traffic": _ncu_traffic(f"{args.config}:gram_matrix")}
     elif cfg.get("thr"):
         vcode = _lib.VARIANTS[used]
         ws = _Workspace(torch, dev, max(_workspace_bytes(lib, code, dm.obs, dm.vars),
@@ -674,11 +685,7 @@ def run_ours(args, cfg, rank, world, dev):
                   if used == "bgram" else f"sweep_kernel[{used}]")
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
-            traffic = json.load(f).get(f"{args.config}:{used}")
+    traffic = _ncu_traffic(f"{args.config}:{used}")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "frac_of_spec_8000": round(achieved / SPEC_HBM_GBS, 4),
                 "peak_source": peak_kind, "traffic": traffic, "kernel": kernel, "kernel_ms": round(k_ms, 4),

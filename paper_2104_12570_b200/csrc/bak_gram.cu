@@ -422,7 +422,7 @@ static int launch_gram_impl(int dtype, const SweepParams& prm, int64_t vars, voi
   // G and the first sweep's g = X^T e (fused into the diagonal-block CTAs)
   const bool fuse_g0 = reinterpret_cast<uintptr_t>(prm.e) % 16 == 0;
   if (int rc = launch_gram_g(dtype, prm.x, prm.obs, prm.ldx, vars, G, gparts_ws, gparts_bytes, st, nullptr,
-                             fuse_g0 ? prm.e : nullptr, fuse_g0 ? gpart : nullptr))
+                             fuse_g0 ? prm.e : nullptr, fuse_g0 ? gpart : nullptr, prm.status))
     return rc;
   BAK_CHECK_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(GramCtrl), st));
 
@@ -637,7 +637,7 @@ extern "C" int bak_solve_gram(int dtype, const void* x, int64_t obs, int64_t var
   BAK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int64_t), st));
   const bool fuse_g0 = reinterpret_cast<uintptr_t>(e) % 16 == 0;
   if (int rc = launch_gram_g(dtype, x, obs, ldx, vars, G, gparts_ws, gparts_bytes, st, norms2_out,
-                             fuse_g0 ? e : nullptr, fuse_g0 ? gpart : nullptr))
+                             fuse_g0 ? e : nullptr, fuse_g0 ? gpart : nullptr, status))
     return rc;
   // all-zero matrix -> the reference's ValueError (bak.py:186-187)
   {

@@ -11,12 +11,18 @@
 // (deterministic) and mirrored.  Diagonal-block CTAs optionally also produce
 // the first sweep's g = X^T e (warp 1, whose quarter of a diagonal block is
 // unused), so the solve skips its first pass over x.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "bak_common.cuh"
 #include "bak_sweep.cuh"
 
 namespace bak {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // bak_gram_tma.cu
+
 namespace {
 
 constexpr int kBT = 64;       // G block edge
@@ -72,6 +78,7 @@ struct GramParams {
   const void* e;                // optional: fused g0 = X^T e in the diagonal CTAs
   double* g0;                   // [cd][vars] per-chunk partials of X^T e
   int* pace;                    // optional: one step counter per CTA (advisory lock step, see below)
+  int64_t* status;              // optional: BAK_ETIMEOUT from the TMA-fed kernel's barrier waits
 };
 
 // off-diagonal block index -> (bi, bj), bi > bj, row-major over the strict lower triangle
@@ -375,6 +382,225 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp64 G, TMA-fed: the same block / chunk / warp-quarter decomposition and the
+// same DMMA order as gram_dmma_kernel<double> (bit-identical partials), but the
+// 16-row x 64-column panels arrive by cp.async.bulk.tensor (2-D tensor map over
+// column-major x, 128B swizzle: a panel column is one 128-byte row, so the
+// m8n8k4 fragment loads — 8 columns x 4 rows per LDS.64 — touch every bank
+// once; rows past obs and columns past vars are zero-filled by the TMA unit)
+// into a 3-stage ring with full / empty mbarriers.  No per-thread address
+// arithmetic, no CTA-wide barrier per stage: a warp waits only for its data,
+// and thread 0 re-arms a slot once the four warps have released it.
+constexpr int kTR = 16;                      // rows per stage: 16 doubles = one 128-byte swizzle row
+constexpr int kTSt = 3;                      // ring depth
+constexpr uint32_t kTTile = kBT * 128;       // bytes per 64-column panel stage
+
+__device__ __forceinline__ void tma_load_2d_g(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_g(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// wait on a phase with the library's deadline; false = timed out (reported, abort flag set)
+__device__ __forceinline__ bool mbar_wait_g(uint64_t* bar, uint32_t parity, volatile int* abort_flag, int64_t* status) {
+  if (mbar_test(bar, parity)) return true;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_test(bar, parity)) {
+    if (*abort_flag) return false;
+    if (globaltimer() - t0 > kTimeoutNs) {
+      report_error(status, BAK_ETIMEOUT);
+      *abort_flag = 1;
+      return false;
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+    gram_dmma_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap emap,
+                         const GramParams p) {
+  extern __shared__ unsigned char smem_raw_t[];
+  const uint32_t base_s = (smem_addr(smem_raw_t) + 1023u) & ~1023u;  // swizzle atoms are 1024-byte aligned
+  unsigned char* base = smem_raw_t + (base_s - smem_addr(smem_raw_t));
+  unsigned char* tiles = base;                                                  // [kTSt][A | B]
+  double* es = reinterpret_cast<double*>(base + kTSt * 2 * kTTile);             // [kTSt][16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kTSt * 2 * kTTile + kTSt * 128);
+  uint64_t* empty = full + kTSt;
+  volatile int* abort_flag = reinterpret_cast<volatile int*>(empty + kTSt);
+
+  const int ndc = p.nb * p.cd;
+  const bool diag = static_cast<int>(blockIdx.x) < ndc;
+  int bi, bj, chk;
+  int64_t chunk;
+  if (diag) {
+    bi = bj = blockIdx.x % p.nb;
+    chk = blockIdx.x / p.nb;
+    chunk = p.chunk_d;
+  } else {
+    const int noff = p.nb * (p.nb - 1) / 2;
+    const int c = blockIdx.x - ndc;
+    tri_index_strict(c % noff, bi, bj);
+    chk = c / noff;
+    chunk = p.chunk_o;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool dq = diag && (warp == 0 || warp == 3);
+  const bool dh = diag && (warp == 1 || warp == 2);
+  const int half = warp == 1 ? 0 : 1;
+  const int wi = dh ? 32 : (warp >> 1) * 32, wj = dh ? 0 : (warp & 1) * 32;
+  const bool with_e = diag && p.e != nullptr;
+  const int64_t k_begin = static_cast<int64_t>(chk) * chunk;
+  const int64_t k_end = imin64(p.obs, k_begin + chunk);
+  const int nsteps = k_end > k_begin ? static_cast<int>((k_end - k_begin + kTR - 1) / kTR) : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < kTSt; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kThreads / 32);
+    }
+    *abort_flag = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const uint32_t stage_bytes = (diag ? kTTile : 2 * kTTile) + (with_e ? kTR * 8u : 0u);
+  auto issue = [&](int step) {
+    const int slot = step % kTSt;
+    const int row0 = static_cast<int>(k_begin + static_cast<int64_t>(step) * kTR);
+    const uint32_t bar = smem_addr(&full[slot]);
+    mbar_arrive_expect_tx(&full[slot], stage_bytes);
+    tma_load_2d_g(smem_addr(tiles + slot * 2 * kTTile), &xmap, row0, bi * kBT, bar);
+    if (!diag) tma_load_2d_g(smem_addr(tiles + slot * 2 * kTTile + kTTile), &xmap, row0, bj * kBT, bar);
+    if (with_e) tma_load_2d_g(smem_addr(es + slot * kTR), &emap, row0, 0, bar);
+  };
+  if (tid == 0)
+    for (int s = 0; s < kTSt - 1 && s < nsteps; ++s) issue(s);
+
+  // advisory lock step of the chunk's CTAs (see gram_dmma_kernel)
+  constexpr int kPaceEvery = BAK_PACE_EVERY, kPaceLead = BAK_PACE_LEAD, kPaceSpins = 200, kPaceDone = 1 << 30;
+  int pace_seen = kPaceDone;
+  const int noff_all = p.nb * (p.nb - 1) / 2;
+  bool paced = p.pace != nullptr;
+  int pace_peer = -1;
+  if (paced && warp == 0) {
+    if (lane < p.nb) pace_peer = chk * p.nb + lane;
+    else if (lane < p.nb + noff_all) pace_peer = ndc + chk * noff_all + (lane - p.nb);
+  }
+
+  double g0a = 0.0;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const int fr = lane >> 2, fk = lane & 3;
+  // byte offset of element (column c, row k) of a panel: c * 128 + (((k >> 1) ^ (c & 7)) << 4) + (k & 1) * 8;
+  // the fragment columns are wi|wj + 8 t + fr, so c & 7 == fr
+  const uint32_t a_row = static_cast<uint32_t>(wi + fr) * 128u, b_row = static_cast<uint32_t>(wj + fr) * 128u;
+  const uint32_t lo8 = static_cast<uint32_t>(fk & 1) * 8u;
+  bool ok = true;
+  for (int step = 0; step < nsteps; ++step) {
+    if (paced && warp == 0) {
+      const int ph = step % kPaceEvery;
+      if (ph == 0) {
+        if (lane == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = step;
+        pace_seen = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
+      } else if (ph == 1) {
+        int v = __reduce_min_sync(0xffffffffu, pace_seen);
+        int spins = 0;
+        while (step > v + kPaceLead) {
+          if (++spins > kPaceSpins) {
+            paced = false;
+            break;
+          }
+          __nanosleep(500);
+          v = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
+          v = __reduce_min_sync(0xffffffffu, v);
+        }
+      }
+    }
+    if (tid == 0) {
+      const int nxt = step + kTSt - 1;
+      if (nxt < nsteps) {
+        // the slot of stage nxt held stage nxt - kTSt: all four warps must have released it
+        if (nxt >= kTSt) ok = mbar_wait_g(&empty[nxt % kTSt], static_cast<uint32_t>((nxt / kTSt - 1) & 1), abort_flag, p.status);
+        if (ok) issue(nxt);
+      }
+    }
+    __syncwarp();
+    const int slot = step % kTSt;
+    if (!mbar_wait_g(&full[slot], static_cast<uint32_t>((step / kTSt) & 1), abort_flag, p.status)) break;
+    const unsigned char* A = tiles + slot * 2 * kTTile;
+    const unsigned char* B = diag ? A : A + kTTile;
+#pragma unroll
+    for (int k4 = 0; k4 < kTR; k4 += 4) {
+      const uint32_t sw = ((static_cast<uint32_t>(k4 >> 1) | static_cast<uint32_t>(fk >> 1)) ^ static_cast<uint32_t>(fr)) << 4;
+      double af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        af[t] = *reinterpret_cast<const double*>(A + a_row + t * 1024 + sw + lo8);
+        bf[t] = *reinterpret_cast<const double*>(B + b_row + t * 1024 + sw + lo8);
+      }
+      if (dq) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b <= a; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      } else if (dh) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if ((a >> 1) == half)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      }
+    }
+    if (with_e && dh) {
+      // fused first-sweep dots, same row order per column as gram_dmma_kernel (lane-rotated)
+      const double* E = es + slot * kTR;
+      const int col = lane + 32 * half;
+      const uint32_t crow = static_cast<uint32_t>(col) * 128u;
+#pragma unroll 8
+      for (int k = 0; k < kTR; ++k) {
+        const int kk = (k + lane) & (kTR - 1);
+        const uint32_t off = crow + ((static_cast<uint32_t>(kk >> 1) ^ static_cast<uint32_t>(col & 7)) << 4) +
+                             static_cast<uint32_t>(kk & 1) * 8u;
+        g0a = __fma_rn(*reinterpret_cast<const double*>(A + off), E[kk], g0a);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_g(&empty[slot]);  // this warp is done reading the slot
+  }
+  if (with_e && dh) {
+    const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane + 32 * half;
+    double* g = p.g0 + static_cast<int64_t>(chk) * p.vars;
+    if (c0 < p.vars) g[c0] = g0a;
+  }
+  if (p.pace && tid == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = kPaceDone;
+  double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (dq ? b > a : (dh && (a >> 1) != half)) continue;
+      const int i = wi + a * 8 + fr, j = wj + b * 8 + fk * 2;
+      out[i * kBT + j] = acc[a][b][0];
+      out[i * kBT + j + 1] = acc[a][b][1];
+    }
+}
+
+constexpr size_t kGramTmaSmem = 1024 + kTSt * 2 * kTTile + kTSt * 128 + 2 * kTSt * 8 + 16;
+
 // G (vars x vars, full, symmetric) = sum over K chunks of the lower block partials
 template <typename T>
 __global__ void gram_reduce_kernel(const double* __restrict__ part, int nb, int cd, int co, int64_t V,
@@ -472,10 +698,20 @@ int64_t gram_g_workspace(int dtype, int64_t obs, int64_t vars, int& nchunks, int
   return ctas * kBT * kBT * 8 + round_up(ctas * 4, 256);  // partials + the pacing counters
 }
 
+// fp64 panels by TMA (default when the tensor map can describe x); BAK_GRAM_G_TMA=0: cp.async kernel
+static bool gram_g_tma_ok(int dtype, const void* x, int64_t obs, int64_t ldx, const void* e) {
+  if (dtype != BAK_F64 || !gram_kt16()) return false;
+  const char* t = getenv("BAK_GRAM_G_TMA");
+  if (t && t[0] == '0') return false;
+  if (reinterpret_cast<uintptr_t>(x) % 16 || (ldx * 8) % 16 || obs >= (int64_t(1) << 31)) return false;
+  if (e && reinterpret_cast<uintptr_t>(e) % 16) return false;
+  return tensor_map_encoder() != nullptr;
+}
+
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
-                  int64_t part_bytes, cudaStream_t st, void* norms_out, const void* e, double* g0) {
+                  int64_t part_bytes, cudaStream_t st, void* norms_out, const void* e, double* g0, int64_t* status) {
   if (gram_tc_enabled(dtype, vars))
-    return launch_gram_g_tc(x, obs, ldx, vars, G, part_ws, part_bytes, st, norms_out, e, g0, nullptr);
+    return launch_gram_g_tc(x, obs, ldx, vars, G, part_ws, part_bytes, st, norms_out, e, g0, status);
   int nchunks;
   int64_t chunk;
   const int64_t need = gram_g_workspace(dtype, obs, vars, nchunks, chunk);
@@ -486,7 +722,7 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   const GramSplit g = gram_split(obs, vars);
   const int nblk = g.nb * (g.nb + 1) / 2;
   GramParams p{x, obs, ldx, vars, g.nb, g.cd, g.co, g.chunk_d, g.chunk_o, static_cast<double*>(part_ws),
-               g0 ? e : nullptr, g0, nullptr};
+               g0 ? e : nullptr, g0, nullptr, status};
   const size_t ts = dtype == BAK_F64 ? 8 : 4;
   const unsigned grid = static_cast<unsigned>(g.nb * g.cd + g.nb * (g.nb - 1) / 2 * g.co);
   // advisory lock step of the CTAs of a K chunk (same rows for every block, <= 32 blocks, one wave);
@@ -510,7 +746,41 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   const bool occ3 = gram_occ() == 3;
   const bool kt16 = gram_kt16();
   int rc;
-  if (kt16) {
+  if (gram_g_tma_ok(dtype, x, obs, ldx, p.e)) {
+    auto enc = tensor_map_encoder();
+    CUtensorMap xmap, emap;
+    {
+      cuuint64_t gdim[2] = {static_cast<cuuint64_t>(obs), static_cast<cuuint64_t>(vars)};
+      cuuint64_t gstr[1] = {static_cast<cuuint64_t>(ldx * 8)};
+      cuuint32_t box[2] = {static_cast<cuuint32_t>(kTR), static_cast<cuuint32_t>(kBT)};
+      cuuint32_t est[2] = {1, 1};
+      CUresult r = enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(x), gdim, gstr, box, est,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (x, fp64 G) failed (%d)", static_cast<int>(r));
+        return BAK_ECUDA;
+      }
+    }
+    {
+      const void* ep = p.e ? p.e : x;  // a valid map either way (unused without e)
+      cuuint64_t gdim[2] = {static_cast<cuuint64_t>(obs), 1};
+      cuuint64_t gstr[1] = {static_cast<cuuint64_t>(round_up(obs * 8, 16))};
+      cuuint32_t box[2] = {static_cast<cuuint32_t>(kTR), 1};
+      cuuint32_t est[2] = {1, 1};
+      CUresult r = enc(&emap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(ep), gdim, gstr, box, est,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (e, fp64 G) failed (%d)", static_cast<int>(r));
+        return BAK_ECUDA;
+      }
+    }
+    BAK_CHECK_CUDA(cudaFuncSetAttribute(gram_dmma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kGramTmaSmem)));
+    gram_dmma_tma_kernel<<<grid, kThreads, kGramTmaSmem, st>>>(xmap, emap, p);
+    rc = BAK_OK;
+  } else if (kt16) {
     auto go16 = [&](auto kern) -> int {
       const size_t smem = 2ull * 2 * kBT * (16 + 4) * ts;
       BAK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -77,7 +77,7 @@ int launch_gram_g_tc(const void* x, int64_t obs, int64_t ldx, int64_t vars, doub
                      int64_t* status);
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
                   int64_t part_bytes, cudaStream_t st, void* norms_out = nullptr, const void* e = nullptr,
-                  double* g0 = nullptr);
+                  double* g0 = nullptr, int64_t* status = nullptr);
 bool gram_tma_supported(int64_t vars);
 int gram_tma_grid(int dtype);
 int launch_gram_pass_tma(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, void* e,

@@ -1,4 +1,5 @@
-"""A/B of the fp64 G kernel's advisory lock step (BAK_GRAM_PACE=0|1) on C3's
+"""A/B of the fp64 G kernel: TMA-fed vs cp.async panels (TMAS="0 1" -> BAK_GRAM_G_TMA) and the advisory
+lock step (PACES -> BAK_GRAM_PACE=0|1) on C3's
 shape: median kernel time of bak_gram_matrix_dot and a G checksum (the result
 must not depend on the pacing).  Tuning aid, not a bench line."""
 import ctypes
@@ -21,8 +22,10 @@ x = torch.randn(nv, obs, dtype=torch.float64, device=dev)
 e = torch.randn(obs, dtype=torch.float64, device=dev)
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ref = None
-for pace in os.environ.get("PACES", "0 1 0 1").split():
+runs = [(t, q) for t in os.environ.get("TMAS", "1").split() for q in os.environ.get("PACES", "0 1 0 1").split()]
+for tma, pace in runs:
     os.environ["BAK_GRAM_PACE"] = pace
+    os.environ["BAK_GRAM_G_TMA"] = tma  # 1: TMA-fed fp64 G kernel (default), 0: cp.async kernel
     G = torch.zeros(nv, nv, dtype=torch.float64, device=dev)
     g0 = torch.zeros(1024, nv, dtype=torch.float64, device=dev)
     wsb = lib.bak_gram_matrix_workspace(code, obs, nv)
@@ -45,5 +48,8 @@ for pace in os.environ.get("PACES", "0 1 0 1").split():
         ts.append(a.elapsed_time(b))
     if ref is None:
         ref = G.clone()
-    print(json.dumps({"pace": pace, "obs": obs, "vars": nv, "ms_median": sorted(ts)[len(ts) // 2], "ms": [round(t, 3) for t in ts],
-                      "bit_identical_to_first": bool(torch.equal(G, ref))}), flush=True)
+    g0sum = g0.sum(0)
+    if ref is not None and "g0ref" not in globals():
+        pass
+    print(json.dumps({"tma": tma, "pace": pace, "obs": obs, "vars": nv, "ms_median": sorted(ts)[len(ts) // 2], "ms": [round(t, 3) for t in ts],
+                      "bit_identical_to_first": bool(torch.equal(G, ref)), "g0_checksum": float(g0sum.abs().sum())}), flush=True)

@@ -79,6 +79,7 @@ struct GramParams {
   double* g0;                   // [cd][vars] per-chunk partials of X^T e
   int* pace;                    // optional: one step counter per CTA (advisory lock step, see below)
   int64_t* status;              // optional: BAK_ETIMEOUT from the TMA-fed kernel's barrier waits
+  int pace_offdiag_only;        // lock step among the off-diagonal CTAs of a chunk only (diagonal CTAs run free)
 };
 
 // off-diagonal block index -> (bi, bj), bi > bj, row-major over the strict lower triangle
@@ -485,14 +486,16 @@ __global__ void __launch_bounds__(kThreads, 4)
   constexpr int kPaceEvery = BAK_PACE_EVERY, kPaceLead = BAK_PACE_LEAD, kPaceSpins = 200, kPaceDone = 1 << 30;
   int pace_seen = kPaceDone;
   const int noff_all = p.nb * (p.nb - 1) / 2;
-  bool paced = p.pace != nullptr;
+  // pace_offdiag_only: 1 = diagonal CTAs run free, 2 = diagonal CTAs follow the off-diagonal ones
+  // (nobody waits for a diagonal CTA)
+  bool paced = p.pace != nullptr && !(p.pace_offdiag_only == 1 && diag);
   int pace_peer = -1;
   if (paced && warp == 0) {
-    if (lane < p.nb) pace_peer = chk * p.nb + lane;
+    if (lane < p.nb) pace_peer = p.pace_offdiag_only ? -1 : chk * p.nb + lane;
     else if (lane < p.nb + noff_all) pace_peer = ndc + chk * noff_all + (lane - p.nb);
   }
 
-  double g0a = 0.0;
+  double g0q[4] = {0.0, 0.0, 0.0, 0.0};
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -566,16 +569,19 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
     }
     if (with_e && dh) {
-      // fused first-sweep dots, same row order per column as gram_dmma_kernel (lane-rotated)
+      // fused first-sweep dots (warps 1-2: column lane + 32 half, rows in a lane-rotated order) as
+      // four independent FMA chains: a DFMA queues behind the DMMAs of 16 warps on the same pipe, and
+      // one 16-long dependent chain per stage made the diagonal CTAs the slowest of their chunk
+      // (40.4 -> 38.6 ms; spreading the dots over all four warps instead: 39.8)
       const double* E = es + slot * kTR;
       const int col = lane + 32 * half;
       const uint32_t crow = static_cast<uint32_t>(col) * 128u;
-#pragma unroll 8
+#pragma unroll
       for (int k = 0; k < kTR; ++k) {
         const int kk = (k + lane) & (kTR - 1);
         const uint32_t off = crow + ((static_cast<uint32_t>(kk >> 1) ^ static_cast<uint32_t>(col & 7)) << 4) +
                              static_cast<uint32_t>(kk & 1) * 8u;
-        g0a = __fma_rn(*reinterpret_cast<const double*>(A + off), E[kk], g0a);
+        g0q[k & 3] = __fma_rn(*reinterpret_cast<const double*>(A + off), E[kk], g0q[k & 3]);
       }
     }
     __syncwarp();
@@ -584,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (with_e && dh) {
     const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane + 32 * half;
     double* g = p.g0 + static_cast<int64_t>(chk) * p.vars;
-    if (c0 < p.vars) g[c0] = g0a;
+    if (c0 < p.vars) g[c0] = (g0q[0] + g0q[1]) + (g0q[2] + g0q[3]);
   }
   if (p.pace && tid == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = kPaceDone;
   double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
@@ -665,7 +671,7 @@ static GramSplit gram_split(int64_t obs, int64_t vars) {
   const int slots = gram_occ() * device_sms();
   const char* rr = getenv("BAK_GRAM_DIAG_RATIO");
   const double ratio = rr ? atof(rr) : 1.0;
-  if (!(ratio > 0.0 && ratio < 1.0)) {
+  if (!(ratio > 0.0 && ratio < 4.0) || ratio == 1.0) {
     g.cd = g.co = imax_host(1, slots / (g.nb * (g.nb + 1) / 2));
   } else if (noff == 0) {
     g.co = 1;
@@ -722,7 +728,7 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   const GramSplit g = gram_split(obs, vars);
   const int nblk = g.nb * (g.nb + 1) / 2;
   GramParams p{x, obs, ldx, vars, g.nb, g.cd, g.co, g.chunk_d, g.chunk_o, static_cast<double*>(part_ws),
-               g0 ? e : nullptr, g0, nullptr, status};
+               g0 ? e : nullptr, g0, nullptr, status, 0};
   const size_t ts = dtype == BAK_F64 ? 8 : 4;
   const unsigned grid = static_cast<unsigned>(g.nb * g.cd + g.nb * (g.nb - 1) / 2 * g.co);
   // advisory lock step of the CTAs of a K chunk (same rows for every block, <= 32 blocks, one wave);
@@ -730,6 +736,7 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   {
     const char* pe = getenv("BAK_GRAM_PACE");
     const bool off = pe && pe[0] == '0';
+    p.pace_offdiag_only = (pe && pe[0] == '2') ? 1 : (pe && pe[0] == '3') ? 2 : 0;
     const int nblk_all = g.nb * (g.nb + 1) / 2;
     if (!off && g.nb > 1 && nblk_all <= 32 && g.cd == g.co && g.chunk_d == g.chunk_o &&
         static_cast<int>(grid) <= gram_occ() * device_sms()) {

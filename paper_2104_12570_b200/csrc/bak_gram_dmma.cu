@@ -80,6 +80,7 @@ struct GramParams {
   int* pace;                    // optional: one step counter per CTA (advisory lock step, see below)
   int64_t* status;              // optional: BAK_ETIMEOUT from the TMA-fed kernel's barrier waits
   int pace_offdiag_only;        // lock step among the off-diagonal CTAs of a chunk only (diagonal CTAs run free)
+  int units;                    // TMA kernel: 1 = two units (off-diagonal, then diagonal) per CTA
 };
 
 // off-diagonal block index -> (bi, bj), bi > bj, row-major over the strict lower triangle
@@ -434,31 +435,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint64_t* empty = full + kTSt;
   volatile int* abort_flag = reinterpret_cast<volatile int*>(empty + kTSt);
 
-  const int ndc = p.nb * p.cd;
-  const bool diag = static_cast<int>(blockIdx.x) < ndc;
-  int bi, bj, chk;
-  int64_t chunk;
-  if (diag) {
-    bi = bj = blockIdx.x % p.nb;
-    chk = blockIdx.x / p.nb;
-    chunk = p.chunk_d;
-  } else {
-    const int noff = p.nb * (p.nb - 1) / 2;
-    const int c = blockIdx.x - ndc;
-    tri_index_strict(c % noff, bi, bj);
-    chk = c / noff;
-    chunk = p.chunk_o;
-  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool dq = diag && (warp == 0 || warp == 3);
-  const bool dh = diag && (warp == 1 || warp == 2);
-  const int half = warp == 1 ? 0 : 1;
-  const int wi = dh ? 32 : (warp >> 1) * 32, wj = dh ? 0 : (warp & 1) * 32;
-  const bool with_e = diag && p.e != nullptr;
-  const int64_t k_begin = static_cast<int64_t>(chk) * chunk;
-  const int64_t k_end = imin64(p.obs, k_begin + chunk);
-  const int nsteps = k_end > k_begin ? static_cast<int>((k_end - k_begin + kTR - 1) / kTR) : 0;
-
   if (tid == 0) {
     for (int s = 0; s < kTSt; ++s) {
       mbar_init(&full[s], 1);
@@ -469,140 +446,192 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
   __syncthreads();
 
-  const uint32_t stage_bytes = (diag ? kTTile : 2 * kTTile) + (with_e ? kTR * 8u : 0u);
-  auto issue = [&](int step) {
-    const int slot = step % kTSt;
-    const int row0 = static_cast<int>(k_begin + static_cast<int64_t>(step) * kTR);
-    const uint32_t bar = smem_addr(&full[slot]);
-    mbar_arrive_expect_tx(&full[slot], stage_bytes);
-    tma_load_2d_g(smem_addr(tiles + slot * 2 * kTTile), &xmap, row0, bi * kBT, bar);
-    if (!diag) tma_load_2d_g(smem_addr(tiles + slot * 2 * kTTile + kTTile), &xmap, row0, bj * kBT, bar);
-    if (with_e) tma_load_2d_g(smem_addr(es + slot * kTR), &emap, row0, 0, bar);
-  };
-  if (tid == 0)
-    for (int s = 0; s < kTSt - 1 && s < nsteps; ++s) issue(s);
-
-  // advisory lock step of the chunk's CTAs (see gram_dmma_kernel)
-  constexpr int kPaceEvery = BAK_PACE_EVERY, kPaceLead = BAK_PACE_LEAD, kPaceSpins = 200, kPaceDone = 1 << 30;
-  int pace_seen = kPaceDone;
+  const int ndc = p.nb * p.cd;
   const int noff_all = p.nb * (p.nb - 1) / 2;
-  // pace_offdiag_only: 1 = diagonal CTAs run free, 2 = diagonal CTAs follow the off-diagonal ones
-  // (nobody waits for a diagonal CTA)
-  bool paced = p.pace != nullptr && !(p.pace_offdiag_only == 1 && diag);
-  int pace_peer = -1;
-  if (paced && warp == 0) {
-    if (lane < p.nb) pace_peer = p.pace_offdiag_only ? -1 : chk * p.nb + lane;
-    else if (lane < p.nb + noff_all) pace_peer = ndc + chk * noff_all + (lane - p.nb);
-  }
-
-  double g0q[4] = {0.0, 0.0, 0.0, 0.0};
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
   const int fr = lane >> 2, fk = lane & 3;
-  // byte offset of element (column c, row k) of a panel: c * 128 + (((k >> 1) ^ (c & 7)) << 4) + (k & 1) * 8;
-  // the fragment columns are wi|wj + 8 t + fr, so c & 7 == fr
-  const uint32_t a_row = static_cast<uint32_t>(wi + fr) * 128u, b_row = static_cast<uint32_t>(wj + fr) * 128u;
   const uint32_t lo8 = static_cast<uint32_t>(fk & 1) * 8u;
-  bool ok = true;
-  for (int step = 0; step < nsteps; ++step) {
+  constexpr int kPaceEvery = BAK_PACE_EVERY, kPaceLead = BAK_PACE_LEAD, kPaceSpins = 200, kPaceDone = 1 << 30;
+
+  // p.units: every CTA runs TWO units — an off-diagonal (block, chunk) and then a diagonal one
+  // (grid = nb * cd = noff * co) — so that all CTAs, and with them all SMs, carry the same work
+  // (one unit per CTA left the SMs that drew two light diagonal CTAs idle at the end: DMMA pipe
+  // 64-90 % active across SMs).  Unit ids and the partial / g0 layout are those of the
+  // one-unit-per-CTA grid, so the reduction is unchanged.  The ring runs on across the units
+  // (gbase = stages issued so far).
+  int gbase = 0;
+  const int nunits = p.units ? 2 : 1;
+  for (int unit = 0; unit < nunits; ++unit) {
+    const int vid = p.units ? (unit == 0 ? ndc + static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x))
+                            : static_cast<int>(blockIdx.x);
+    const bool diag = vid < ndc;
+    int bi, bj, chk;
+    int64_t chunk;
+    if (diag) {
+      bi = bj = vid % p.nb;
+      chk = vid / p.nb;
+      chunk = p.chunk_d;
+    } else {
+      const int c = vid - ndc;
+      tri_index_strict(c % noff_all, bi, bj);
+      chk = c / noff_all;
+      chunk = p.chunk_o;
+    }
+    const bool dq = diag && (warp == 0 || warp == 3);
+    const bool dh = diag && (warp == 1 || warp == 2);
+    const int half = warp == 1 ? 0 : 1;
+    const int wi = dh ? 32 : (warp >> 1) * 32, wj = dh ? 0 : (warp & 1) * 32;
+    const bool with_e = diag && p.e != nullptr;
+    const int64_t k_begin = static_cast<int64_t>(chk) * chunk;
+    const int64_t k_end = imin64(p.obs, k_begin + chunk);
+    const int nsteps = k_end > k_begin ? static_cast<int>((k_end - k_begin + kTR - 1) / kTR) : 0;
+
+    const uint32_t stage_bytes = (diag ? kTTile : 2 * kTTile) + (with_e ? kTR * 8u : 0u);
+    // thread 0: arm the slot of global stage gbase + step (after its previous use has been released
+    // by all four warps) and start the copies
+    auto issue = [&](int step) -> bool {
+      const int g = gbase + step;
+      const int slot = g % kTSt;
+      if (g >= kTSt &&
+          !mbar_wait_g(&empty[slot], static_cast<uint32_t>((g / kTSt - 1) & 1), abort_flag, p.status))
+        return false;
+      const int row0 = static_cast<int>(k_begin + static_cast<int64_t>(step) * kTR);
+      const uint32_t bar = smem_addr(&full[slot]);
+      mbar_arrive_expect_tx(&full[slot], stage_bytes);
+      tma_load_2d_g(smem_addr(tiles + slot * 2 * kTTile), &xmap, row0, bi * kBT, bar);
+      if (!diag) tma_load_2d_g(smem_addr(tiles + slot * 2 * kTTile + kTTile), &xmap, row0, bj * kBT, bar);
+      if (with_e) tma_load_2d_g(smem_addr(es + slot * kTR), &emap, row0, 0, bar);
+      return true;
+    };
+    if (tid == 0)
+      for (int s = 0; s < kTSt - 1 && s < nsteps; ++s)
+        if (!issue(s)) break;
+
+    // advisory lock step of the CTAs that read the same rows (see gram_dmma_kernel); counters are
+    // indexed by CTA.  pace_offdiag_only: 1 = diagonal units run free, 2 = they follow the
+    // off-diagonal ones; with two units per CTA only the off-diagonal units share rows in time.
+    int pace_seen = kPaceDone;
+    bool paced = p.pace != nullptr && !((p.pace_offdiag_only == 1 || p.units) && diag);
+    int pace_peer = -1;
     if (paced && warp == 0) {
-      const int ph = step % kPaceEvery;
-      if (ph == 0) {
-        if (lane == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = step;
-        pace_seen = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
-      } else if (ph == 1) {
-        int v = __reduce_min_sync(0xffffffffu, pace_seen);
-        int spins = 0;
-        while (step > v + kPaceLead) {
-          if (++spins > kPaceSpins) {
-            paced = false;
-            break;
+      if (p.units) {
+        if (lane < noff_all) pace_peer = chk * noff_all + lane;
+      } else if (lane < p.nb) {
+        pace_peer = p.pace_offdiag_only ? -1 : chk * p.nb + lane;
+      } else if (lane < p.nb + noff_all) {
+        pace_peer = ndc + chk * noff_all + (lane - p.nb);
+      }
+    }
+
+    double g0q[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    // byte offset of element (column c, row k) of a panel: c * 128 + (((k >> 1) ^ (c & 7)) << 4) + (k & 1) * 8;
+    // the fragment columns are wi|wj + 8 t + fr, so c & 7 == fr
+    const uint32_t a_row = static_cast<uint32_t>(wi + fr) * 128u, b_row = static_cast<uint32_t>(wj + fr) * 128u;
+    bool alive = true;
+    for (int step = 0; step < nsteps; ++step) {
+      if (paced && warp == 0) {
+        const int ph = step % kPaceEvery;
+        if (ph == 0) {
+          if (lane == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = step;
+          pace_seen = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
+        } else if (ph == 1) {
+          int v = __reduce_min_sync(0xffffffffu, pace_seen);
+          int spins = 0;
+          while (step > v + kPaceLead) {
+            if (++spins > kPaceSpins) {
+              paced = false;
+              break;
+            }
+            __nanosleep(500);
+            v = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
+            v = __reduce_min_sync(0xffffffffu, v);
           }
-          __nanosleep(500);
-          v = pace_peer >= 0 ? *reinterpret_cast<volatile const int*>(p.pace + pace_peer) : kPaceDone;
-          v = __reduce_min_sync(0xffffffffu, v);
         }
       }
-    }
-    if (tid == 0) {
-      const int nxt = step + kTSt - 1;
-      if (nxt < nsteps) {
-        // the slot of stage nxt held stage nxt - kTSt: all four warps must have released it
-        if (nxt >= kTSt) ok = mbar_wait_g(&empty[nxt % kTSt], static_cast<uint32_t>((nxt / kTSt - 1) & 1), abort_flag, p.status);
-        if (ok) issue(nxt);
+      if (tid == 0) {
+        const int nxt = step + kTSt - 1;
+        if (nxt < nsteps) issue(nxt);
       }
-    }
-    __syncwarp();
-    const int slot = step % kTSt;
-    if (!mbar_wait_g(&full[slot], static_cast<uint32_t>((step / kTSt) & 1), abort_flag, p.status)) break;
-    const unsigned char* A = tiles + slot * 2 * kTTile;
-    const unsigned char* B = diag ? A : A + kTTile;
-#pragma unroll
-    for (int k4 = 0; k4 < kTR; k4 += 4) {
-      const uint32_t sw = ((static_cast<uint32_t>(k4 >> 1) | static_cast<uint32_t>(fk >> 1)) ^ static_cast<uint32_t>(fr)) << 4;
-      double af[4], bf[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        af[t] = *reinterpret_cast<const double*>(A + a_row + t * 1024 + sw + lo8);
-        bf[t] = *reinterpret_cast<const double*>(B + b_row + t * 1024 + sw + lo8);
+      __syncwarp();
+      const int g = gbase + step;
+      const int slot = g % kTSt;
+      if (!mbar_wait_g(&full[slot], static_cast<uint32_t>((g / kTSt) & 1), abort_flag, p.status)) {
+        alive = false;
+        break;
       }
-      if (dq) {
+      const unsigned char* A = tiles + slot * 2 * kTTile;
+      const unsigned char* B = diag ? A : A + kTTile;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+      for (int k4 = 0; k4 < kTR; k4 += 4) {
+        const uint32_t sw = ((static_cast<uint32_t>(k4 >> 1) | static_cast<uint32_t>(fk >> 1)) ^ static_cast<uint32_t>(fr)) << 4;
+        double af[4], bf[4];
 #pragma unroll
-          for (int b = 0; b <= a; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-      } else if (dh) {
+        for (int t = 0; t < 4; ++t) {
+          af[t] = *reinterpret_cast<const double*>(A + a_row + t * 1024 + sw + lo8);
+          bf[t] = *reinterpret_cast<const double*>(B + b_row + t * 1024 + sw + lo8);
+        }
+        if (dq) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-          if ((a >> 1) == half)
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        } else if (dh) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            if ((a >> 1) == half)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-      } else {
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
       }
+      if (with_e && dh) {
+        // fused first-sweep dots (warps 1-2: column lane + 32 half, rows in a lane-rotated order) as
+        // four independent FMA chains: a DFMA queues behind the DMMAs of 16 warps on the same pipe, and
+        // one 16-long dependent chain per stage made the diagonal CTAs the slowest of their chunk
+        // (40.4 -> 38.6 ms; spreading the dots over all four warps instead: 39.8)
+        const double* E = es + slot * kTR;
+        const int col = lane + 32 * half;
+        const uint32_t crow = static_cast<uint32_t>(col) * 128u;
+#pragma unroll
+        for (int k = 0; k < kTR; ++k) {
+          const int kk = (k + lane) & (kTR - 1);
+          const uint32_t off = crow + ((static_cast<uint32_t>(kk >> 1) ^ static_cast<uint32_t>(col & 7)) << 4) +
+                               static_cast<uint32_t>(kk & 1) * 8u;
+          g0q[k & 3] = __fma_rn(*reinterpret_cast<const double*>(A + off), E[kk], g0q[k & 3]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_g(&empty[slot]);  // this warp is done reading the slot
     }
     if (with_e && dh) {
-      // fused first-sweep dots (warps 1-2: column lane + 32 half, rows in a lane-rotated order) as
-      // four independent FMA chains: a DFMA queues behind the DMMAs of 16 warps on the same pipe, and
-      // one 16-long dependent chain per stage made the diagonal CTAs the slowest of their chunk
-      // (40.4 -> 38.6 ms; spreading the dots over all four warps instead: 39.8)
-      const double* E = es + slot * kTR;
-      const int col = lane + 32 * half;
-      const uint32_t crow = static_cast<uint32_t>(col) * 128u;
+      const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane + 32 * half;
+      double* g = p.g0 + static_cast<int64_t>(chk) * p.vars;
+      if (c0 < p.vars) g[c0] = (g0q[0] + g0q[1]) + (g0q[2] + g0q[3]);
+    }
+    if (p.pace && tid == 0 && (unit == nunits - 1 || !diag))
+      *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = kPaceDone;
+    double* out = p.part + static_cast<size_t>(vid) * kBT * kBT;
 #pragma unroll
-      for (int k = 0; k < kTR; ++k) {
-        const int kk = (k + lane) & (kTR - 1);
-        const uint32_t off = crow + ((static_cast<uint32_t>(kk >> 1) ^ static_cast<uint32_t>(col & 7)) << 4) +
-                             static_cast<uint32_t>(kk & 1) * 8u;
-        g0q[k & 3] = __fma_rn(*reinterpret_cast<const double*>(A + off), E[kk], g0q[k & 3]);
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (dq ? b > a : (dh && (a >> 1) != half)) continue;
+        const int i = wi + a * 8 + fr, j = wj + b * 8 + fk * 2;
+        out[i * kBT + j] = acc[a][b][0];
+        out[i * kBT + j + 1] = acc[a][b][1];
       }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_g(&empty[slot]);  // this warp is done reading the slot
+    if (!alive) break;
+    gbase += nsteps;
   }
-  if (with_e && dh) {
-    const int64_t c0 = static_cast<int64_t>(bi) * kBT + lane + 32 * half;
-    double* g = p.g0 + static_cast<int64_t>(chk) * p.vars;
-    if (c0 < p.vars) g[c0] = (g0q[0] + g0q[1]) + (g0q[2] + g0q[3]);
-  }
-  if (p.pace && tid == 0) *reinterpret_cast<volatile int*>(p.pace + blockIdx.x) = kPaceDone;
-  double* out = p.part + static_cast<size_t>(blockIdx.x) * kBT * kBT;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (dq ? b > a : (dh && (a >> 1) != half)) continue;
-      const int i = wi + a * 8 + fr, j = wj + b * 8 + fk * 2;
-      out[i * kBT + j] = acc[a][b][0];
-      out[i * kBT + j + 1] = acc[a][b][1];
-    }
 }
 
 constexpr size_t kGramTmaSmem = 1024 + kTSt * 2 * kTTile + kTSt * 128 + 2 * kTSt * 8 + 16;
@@ -640,6 +669,7 @@ static inline int imax_host(int a, int b) { return a > b ? a : b; }
 struct GramSplit {
   int nb, cd, co;
   int64_t chunk_d, chunk_o;
+  int units;  // TMA-fed fp64 kernel: two units per CTA (grid = nb * cd = noff * co)
 };
 
 // CTAs per SM of the G kernel: 3 (2-stage ring, <=170 registers) keeps the DMMA
@@ -658,10 +688,43 @@ static int gram_occ() {
   return (o && o[0] == '2') ? 2 : 3;
 }
 
-static GramSplit gram_split(int64_t obs, int64_t vars) {
+// the TMA-fed fp64 kernel can be used (x / e alignment is checked at launch; misaligned inputs run the
+// cp.async kernel on the same split); BAK_GRAM_G_TMA=0: cp.async kernel
+static bool gram_g_tma_wanted(int dtype, int64_t obs) {
+  if (dtype != BAK_F64 || !gram_kt16() || obs >= (int64_t(1) << 31)) return false;
+  const char* t = getenv("BAK_GRAM_G_TMA");
+  if (t && t[0] == '0') return false;
+  return tensor_map_encoder() != nullptr;
+}
+
+static int64_t gcd64(int64_t a, int64_t b) { return b ? gcd64(b, a % b) : a; }
+
+static GramSplit gram_split(int dtype, int64_t obs, int64_t vars) {
   GramSplit g{};
   g.nb = static_cast<int>((vars + kBT - 1) / kBT);
   const int noff = g.nb * (g.nb - 1) / 2;
+  {
+    // BAK_GRAM_UNITS=1 (tuning aid, off by default): two units per CTA — U CTAs, U the largest multiple
+    // of lcm(nb, noff) in one wave; diagonal block b of chunk c is unit c * nb + b, off-diagonal block o
+    // of chunk c is c * noff + o.  Every SM then carries the same work: 38.6 vs 39.6 ms alone on C3's
+    // shape, but the diagonal and off-diagonal units of a row range no longer run together, so x comes
+    // from DRAM 2-2.8 times (72-96 GB), and inside the power-capped C3 step it measured the same
+    // 132-133 sweeps/s as one unit per CTA in full lock step (35 GB) — which is therefore the default.
+    const char* u = getenv("BAK_GRAM_UNITS");
+    const int slots4 = 4 * device_sms();
+    if ((u && u[0] == '1') && !getenv("BAK_GRAM_DIAG_RATIO") && noff > 0 && gram_g_tma_wanted(dtype, obs)) {
+      const int64_t l = static_cast<int64_t>(g.nb) / gcd64(g.nb, noff) * noff;
+      if (l <= slots4) {
+        const int64_t U = slots4 / l * l;
+        g.units = 1;
+        g.cd = static_cast<int>(U / g.nb);
+        g.co = static_cast<int>(U / noff);
+        g.chunk_d = round_up((obs + g.cd - 1) / g.cd, kKT);
+        g.chunk_o = round_up((obs + g.co - 1) / g.co, kKT);
+        return g;  // chunks past obs stay in the grid (they write zero partials)
+      }
+    }
+  }
   // One wave of CTAs, equal row chunks for every block by default.  With the
   // first sweep's dots fused (warps 1-2 of the diagonal CTAs), diagonal and
   // off-diagonal CTAs then take about the same time (in-solve G on C3: 42.8 ms
@@ -697,21 +760,18 @@ int64_t gram_g_workspace(int dtype, int64_t obs, int64_t vars, int& nchunks, int
     chunk = obs;
     return gram_tc_workspace(obs, vars);
   }
-  const GramSplit g = gram_split(obs, vars);
+  const GramSplit g = gram_split(dtype, obs, vars);
   nchunks = g.cd;  // partial rows of the fused g0
   chunk = g.chunk_d;
   const int64_t ctas = static_cast<int64_t>(g.nb) * g.cd + static_cast<int64_t>(g.nb) * (g.nb - 1) / 2 * g.co;
   return ctas * kBT * kBT * 8 + round_up(ctas * 4, 256);  // partials + the pacing counters
 }
 
-// fp64 panels by TMA (default when the tensor map can describe x); BAK_GRAM_G_TMA=0: cp.async kernel
 static bool gram_g_tma_ok(int dtype, const void* x, int64_t obs, int64_t ldx, const void* e) {
-  if (dtype != BAK_F64 || !gram_kt16()) return false;
-  const char* t = getenv("BAK_GRAM_G_TMA");
-  if (t && t[0] == '0') return false;
-  if (reinterpret_cast<uintptr_t>(x) % 16 || (ldx * 8) % 16 || obs >= (int64_t(1) << 31)) return false;
+  if (!gram_g_tma_wanted(dtype, obs)) return false;
+  if (reinterpret_cast<uintptr_t>(x) % 16 || (ldx * 8) % 16) return false;
   if (e && reinterpret_cast<uintptr_t>(e) % 16) return false;
-  return tensor_map_encoder() != nullptr;
+  return true;
 }
 
 int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t vars, double* G, void* part_ws,
@@ -725,12 +785,16 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
     set_error("gram: partial workspace too small");
     return BAK_EWORKSPACE;
   }
-  const GramSplit g = gram_split(obs, vars);
+  const GramSplit g = gram_split(dtype, obs, vars);
   const int nblk = g.nb * (g.nb + 1) / 2;
   GramParams p{x, obs, ldx, vars, g.nb, g.cd, g.co, g.chunk_d, g.chunk_o, static_cast<double*>(part_ws),
-               g0 ? e : nullptr, g0, nullptr, status, 0};
+               g0 ? e : nullptr, g0, nullptr, status, 0, 0};
   const size_t ts = dtype == BAK_F64 ? 8 : 4;
-  const unsigned grid = static_cast<unsigned>(g.nb * g.cd + g.nb * (g.nb - 1) / 2 * g.co);
+  const bool tma = gram_g_tma_ok(dtype, x, obs, ldx, p.e);
+  const bool units = tma && g.units;
+  p.units = units ? 1 : 0;
+  const unsigned grid = units ? static_cast<unsigned>(g.nb * g.cd)
+                              : static_cast<unsigned>(g.nb * g.cd + g.nb * (g.nb - 1) / 2 * g.co);
   // advisory lock step of the CTAs of a K chunk (same rows for every block, <= 32 blocks, one wave);
   // BAK_GRAM_PACE=0 switches it off
   {
@@ -738,9 +802,10 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
     const bool off = pe && pe[0] == '0';
     p.pace_offdiag_only = (pe && pe[0] == '2') ? 1 : (pe && pe[0] == '3') ? 2 : 0;
     const int nblk_all = g.nb * (g.nb + 1) / 2;
-    if (!off && g.nb > 1 && nblk_all <= 32 && g.cd == g.co && g.chunk_d == g.chunk_o &&
+    const size_t nparts = static_cast<size_t>(g.nb) * g.cd + static_cast<size_t>(g.nb) * (g.nb - 1) / 2 * g.co;
+    if (!off && g.nb > 1 && nblk_all <= 32 && (units || (g.cd == g.co && g.chunk_d == g.chunk_o)) &&
         static_cast<int>(grid) <= gram_occ() * device_sms()) {
-      p.pace = reinterpret_cast<int*>(static_cast<char*>(part_ws) + static_cast<size_t>(grid) * kBT * kBT * 8);
+      p.pace = reinterpret_cast<int*>(static_cast<char*>(part_ws) + nparts * kBT * kBT * 8);
       BAK_CHECK_CUDA(cudaMemsetAsync(p.pace, 0, static_cast<size_t>(grid) * 4, st));
     }
   }
@@ -753,7 +818,7 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
   const bool occ3 = gram_occ() == 3;
   const bool kt16 = gram_kt16();
   int rc;
-  if (gram_g_tma_ok(dtype, x, obs, ldx, p.e)) {
+  if (tma) {
     auto enc = tensor_map_encoder();
     CUtensorMap xmap, emap;
     {

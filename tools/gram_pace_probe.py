@@ -26,6 +26,7 @@ runs = [(t, q) for t in os.environ.get("TMAS", "1").split() for q in os.environ.
 for tma, pace in runs:
     os.environ["BAK_GRAM_PACE"] = pace
     os.environ["BAK_GRAM_G_TMA"] = tma  # 1: TMA-fed fp64 G kernel (default), 0: cp.async kernel
+    # BAK_GRAM_UNITS (0: one unit per CTA, default: two) is read from the caller's environment
     G = torch.zeros(nv, nv, dtype=torch.float64, device=dev)
     g0 = torch.zeros(1024, nv, dtype=torch.float64, device=dev)
     wsb = lib.bak_gram_matrix_workspace(code, obs, nv)

@@ -140,3 +140,39 @@ def test_gram_fp32_3xtf32_on_correlated_columns(corr, monkeypatch):
         rep = pb.solve_bak(x, y, pb.SolveConfig(max_iter=12, tol=0), variant="gram")
         err = orc.rel_coeff_err(rep.a_hat, ref["a_hat"])
         assert rep.sweeps_run == 12 and err <= 1e-4, (corr, env, err)
+
+
+@pytest.mark.parametrize("obs,nv", [(1000, 7), (50_001, 64), (131_071, 130), (200_003, 256), (70_000, 320)])
+def test_gram_matrix_fp64_tma_matches_cp_async_bitwise(obs, nv, monkeypatch):
+    """The TMA-fed fp64 G kernel (default) issues the same DMMAs in the same order as the cp.async
+    kernel (BAK_GRAM_G_TMA=0): identical bits, with or without the advisory lock step, with one or
+    two units per CTA, on ragged rows / columns (zero-filled by the TMA unit)."""
+    x = np.asfortranarray(np.random.default_rng(obs + 7).standard_normal((obs, nv)))
+    base = _gram(x, monkeypatch, {"BAK_GRAM_G_TMA": "0", "BAK_GRAM_PACE": "0"})
+    for env in ({"BAK_GRAM_G_TMA": "1", "BAK_GRAM_PACE": "0", "BAK_GRAM_UNITS": "0"},
+                {"BAK_GRAM_G_TMA": "1", "BAK_GRAM_PACE": "1", "BAK_GRAM_UNITS": "0"},
+                {"BAK_GRAM_G_TMA": "1", "BAK_GRAM_PACE": "3", "BAK_GRAM_UNITS": "0"},
+                {"BAK_GRAM_G_TMA": "0", "BAK_GRAM_PACE": "1", "BAK_GRAM_UNITS": "0"}):
+        G = _gram(x, monkeypatch, env)
+        assert np.array_equal(G, base), env
+    # two units per CTA: other chunk boundaries, so other (fixed-order) sums — same accuracy bar
+    G2 = _gram(x, monkeypatch, {"BAK_GRAM_G_TMA": "1", "BAK_GRAM_PACE": "1", "BAK_GRAM_UNITS": "1"})
+    ref = x.T @ x
+    assert np.linalg.norm(G2 - ref) / np.linalg.norm(ref) <= 1e-13
+    assert np.array_equal(G2, G2.T)
+
+
+def test_gram_fused_first_dots_tma_vs_cp_async(monkeypatch):
+    """GRAM solves through the TMA-fed G kernel (fused first-sweep dots as four FMA chains) and through
+    the cp.async kernel agree to rounding, and both meet the oracle bar."""
+    import paper_2104_12570_b200 as pb
+    from oracle import bak_oracle as orc
+    x, y, _ = orc.config_c3(obs=1 << 16, nvars=96)
+    ref = orc.solve(x, y, max_iter=4, tol=0)
+    out = {}
+    for tma in ("0", "1"):
+        monkeypatch.setenv("BAK_GRAM_G_TMA", tma)
+        r = pb.solve_bak(x, y, pb.SolveConfig(max_iter=4, tol=0), variant="gram")
+        assert orc.rel_coeff_err(r.a_hat, ref["a_hat"]) <= 1e-10
+        out[tma] = np.asarray(r.a_hat, dtype=np.float64)
+    assert np.linalg.norm(out["0"] - out["1"]) <= 1e-13 * np.linalg.norm(out["0"])

@@ -612,7 +612,8 @@ def run_ours(args, cfg, rank, world, dev):
         noff = nb * (nb - 1) // 2
         if ts == 8:  # fp64 DMMA: off-diagonal blocks 64 8x8 tiles, diagonal blocks their 36 lower tiles
             flops = 2.0 * dm.obs * 64 * (64 * noff + 36 * nb)
-            gk, gbound, gpeak = ("gram_dmma_kernel (fp64 DMMA m8n8k4 SYRK, lower 64x64 blocks)",
+            gk, gbound, gpeak = ("gram_dmma_tma_kernel (fp64 DMMA m8n8k4 SYRK over lower 64x64 blocks, panels by TMA "
+                                 "through a 128B-swizzled 3-stage mbarrier ring; BAK_GRAM_G_TMA=0: cp.async kernel)",
                                  "tensor (fp64 DMMA)", DMMA_PEAK_TFLOPS)
             gsrc = "tools/micro/dmma_peak.cu: register-only m8n8k4 f64 DMMA, all SMs, 1965 MHz"
         elif os.environ.get("BAK_GRAM_G", "")[:1] in ("x", "d"):  # legacy mma.sync 3xTF32 kernel

@@ -395,7 +395,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gram_dmma_kernel(const G
 // arithmetic, no CTA-wide barrier per stage: a warp waits only for its data,
 // and thread 0 re-arms a slot once the four warps have released it.
 constexpr int kTR = 16;                      // rows per stage: 16 doubles = one 128-byte swizzle row
-constexpr int kTSt = 3;                      // ring depth
+// ring depth x CTAs per SM: 4 x 3 (66 KB each); 3 x 4 is 0.4 ms (free-running) to 1.2 ms (lock step) slower on C3's
+// shape, 6 x 2 is 10 ms slower (profiles/r02_gram_pace.jsonl)
+#ifndef BAK_GT_STAGES
+#define BAK_GT_STAGES 4
+#endif
+#ifndef BAK_GT_OCC
+#define BAK_GT_OCC 3
+#endif
+constexpr int kTSt = BAK_GT_STAGES;
 constexpr uint32_t kTTile = kBT * 128;       // bytes per 64-column panel stage
 
 __device__ __forceinline__ void tma_load_2d_g(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
@@ -423,7 +431,7 @@ __device__ __forceinline__ bool mbar_wait_g(uint64_t* bar, uint32_t parity, vola
   return true;
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, BAK_GT_OCC)
     gram_dmma_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap emap,
                          const GramParams p) {
   extern __shared__ unsigned char smem_raw_t[];
@@ -690,11 +698,16 @@ static int gram_occ() {
 
 // the TMA-fed fp64 kernel can be used (x / e alignment is checked at launch; misaligned inputs run the
 // cp.async kernel on the same split); BAK_GRAM_G_TMA=0: cp.async kernel
-static bool gram_g_tma_wanted(int dtype, int64_t obs) {
+// (the chunk split below is sized for the TMA-fed kernel whenever it COULD run, so that BAK_GRAM_G_TMA=0
+// gives the cp.async kernel the same chunks and therefore the same bits)
+static bool gram_g_tma_possible(int dtype, int64_t obs) {
   if (dtype != BAK_F64 || !gram_kt16() || obs >= (int64_t(1) << 31)) return false;
+  return tensor_map_encoder() != nullptr;
+}
+static bool gram_g_tma_wanted(int dtype, int64_t obs) {
   const char* t = getenv("BAK_GRAM_G_TMA");
   if (t && t[0] == '0') return false;
-  return tensor_map_encoder() != nullptr;
+  return gram_g_tma_possible(dtype, obs);
 }
 
 static int64_t gcd64(int64_t a, int64_t b) { return b ? gcd64(b, a % b) : a; }
@@ -711,7 +724,7 @@ static GramSplit gram_split(int dtype, int64_t obs, int64_t vars) {
     // from DRAM 2-2.8 times (72-96 GB), and inside the power-capped C3 step it measured the same
     // 132-133 sweeps/s as one unit per CTA in full lock step (35 GB) — which is therefore the default.
     const char* u = getenv("BAK_GRAM_UNITS");
-    const int slots4 = 4 * device_sms();
+    const int slots4 = BAK_GT_OCC * device_sms();
     if ((u && u[0] == '1') && !getenv("BAK_GRAM_DIAG_RATIO") && noff > 0 && gram_g_tma_wanted(dtype, obs)) {
       const int64_t l = static_cast<int64_t>(g.nb) / gcd64(g.nb, noff) * noff;
       if (l <= slots4) {
@@ -731,7 +744,7 @@ static GramSplit gram_split(int dtype, int64_t obs, int64_t vars) {
   // fp64 / 36.2 ms fp32 at ratio 1 vs 46.8 / 43.3 at 0.625 — the 10/16 ratio
   // of their DMMA tiles alone).  BAK_GRAM_DIAG_RATIO=r gives diagonal blocks
   // 1/r of the rows (tuning aid).
-  const int slots = gram_occ() * device_sms();
+  const int slots = (gram_g_tma_possible(dtype, obs) ? BAK_GT_OCC : gram_occ()) * device_sms();
   const char* rr = getenv("BAK_GRAM_DIAG_RATIO");
   const double ratio = rr ? atof(rr) : 1.0;
   if (!(ratio > 0.0 && ratio < 4.0) || ratio == 1.0) {
@@ -804,7 +817,7 @@ int launch_gram_g(int dtype, const void* x, int64_t obs, int64_t ldx, int64_t va
     const int nblk_all = g.nb * (g.nb + 1) / 2;
     const size_t nparts = static_cast<size_t>(g.nb) * g.cd + static_cast<size_t>(g.nb) * (g.nb - 1) / 2 * g.co;
     if (!off && g.nb > 1 && nblk_all <= 32 && (units || (g.cd == g.co && g.chunk_d == g.chunk_o)) &&
-        static_cast<int>(grid) <= gram_occ() * device_sms()) {
+        static_cast<int>(grid) <= (gram_g_tma_possible(dtype, obs) ? BAK_GT_OCC : gram_occ()) * device_sms()) {
       p.pace = reinterpret_cast<int*>(static_cast<char*>(part_ws) + nparts * kBT * kBT * 8);
       BAK_CHECK_CUDA(cudaMemsetAsync(p.pace, 0, static_cast<size_t>(grid) * 4, st));
     }
